@@ -1,0 +1,86 @@
+"""Pins of oracle/partition.py: SPEC worked examples, fairness, plan symmetry, and
+rank-count invariance of the assembled operator (sum of per-rank partial applies)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import basis, mesh, operator, partition
+from tests.inputs import uniform_vector
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def test_rank_grid_examples():
+    for P, box, expect in gold("partition.json")["rank_grid"]:
+        assert partition.rank_grid(P, *box) == tuple(expect)
+    with pytest.raises(ValueError):
+        partition.rank_grid(7, 2, 2, 2)
+
+
+def test_classify_examples():
+    for c in gold("partition.json")["classify"]:
+        ranks = partition.build(*c["box"], c["N"], c["P"])
+        for r in ranks:
+            assert r["nH"] == c["halo"] and r["nA"] == c["A"] and r["nB"] == c["B"]
+        if "shared_nodes" in c:
+            assert len(ranks[0]["send"].get(1, [])) + len(ranks[0]["recv"].get(1, [])) == c["shared_nodes"]
+
+
+def test_axis_remainder_goes_to_low_ranks():
+    assert partition.axis_owner(7, 3) == [0, 0, 0, 1, 1, 2, 2]
+
+
+@pytest.mark.parametrize("box,N,P", [((4, 4, 4), 3, 2), ((3, 2, 2), 2, 4), ((2, 2, 2), 1, 8), ((5, 3, 2), 2, 3)])
+def test_partition_invariants(box, N, P):
+    ranks = partition.build(*box, N, P, seed=0)
+    E, NG, NL = mesh.global_sizes(*box, N)
+    owned = np.concatenate([np.array(r["owned"], dtype=np.int64) for r in ranks])
+    assert np.array_equal(np.sort(owned), np.arange(NG))           # each gid owned exactly once
+    assert sorted(e for r in ranks for e in r["elements"]) == list(range(E))
+    for q, r in enumerate(ranks):
+        assert r["nA"] + r["nH"] + r["nB"] == len(r["elements"])
+        for p_ in r["neighbors"]:
+            assert q in ranks[p_]["neighbors"]                      # symmetric neighbour sets
+            assert r["send"][p_] == ranks[p_]["recv"][q]           # plan symmetry
+        # owner is one of the sharers: every halo gid is referenced by me and owned elsewhere
+        ext = r["owned"] + r["halo"]
+        assert np.array_equal(np.array(ext)[r["idx"]], r["gid"])
+
+
+def test_ownership_fairness():
+    """1000 nodes shared by 2 ranks: owner counts within [400, 600]."""
+    from oracle.forcing import splitmix64
+    h = splitmix64(0)
+    own = [splitmix64(h ^ g) % 2 for g in range(1000)]
+    assert 400 <= sum(own) <= 600
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_rank_count_invariance_of_apply(P):
+    """Sum over ranks of Z_r^T (S_L + lambda W) Z_r x (each rank's elements) equals the
+    P=1 apply, and the owner-assembled result is identical."""
+    box, N = (4, 2, 2), 3
+    x, w, D = basis.basis(N)
+    E, NG, NL = mesh.global_sizes(*box, N)
+    gid = mesh.l2g(*box, N)
+    G = mesh.geometric_factors(E, N, w)
+    W = mesh.weights_W(gid, NG)
+    xv = uniform_vector(NG, 4)
+    ref = operator.apply(xv, gid, D, G, 1.0, W)
+    ranks = partition.build(*box, N, P)
+    total = np.zeros(NG)
+    for r in ranks:
+        el = r["elements"]
+        ext = np.array(r["owned"] + r["halo"], dtype=np.int64)
+        u = xv[ext][r["idx"]]
+        y = operator.local_apply(D, G[el], u) + W[el] * u
+        part = np.bincount(r["idx"].ravel(), weights=y.ravel(), minlength=len(ext))
+        total[ext] += part
+    assert np.max(np.abs(total - ref)) < 1e-13 * np.max(np.abs(ref))
