@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""hipBone hot-path benchmark on B200 (BASELINE.json metric: CG GFLOP/s in the NekBone count
+& operator HBM GB/s vs peak at N=7).
+
+A step = one fixed-iteration CG solve (Alg. 1; 100 iterations) from x0 = 0 on
+the synthetic box workload, i.e. every §8(a) row: gather, gradient, metric, divergence,
+scatter-add (operator), p.Ap, r/x update + r.r, p update.  Default workload C2 (N=7, 16^3
+elements, BASELINE.json configs[1]); with --gpus P > 1 every rank gets a C2-sized block of a
+(16 px) x (16 py) x (16 pz) box (weak scaling, C4 shape).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--box 16,16,16] [--N 7]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the CPU oracle (oracle/, plain numpy fp64) on a bounded sample of the
+same workload -- the tier's reference arm.  Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CG GFLOP/s (NekBone count) & operator HBM GB/s vs peak at N=7"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--box", default="16,16,16", help="elements per rank (per-rank block for P>1)")
+    ap.add_argument("--N", type=int, default=7)
+    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-profile", action="store_true", help="do not bracket operator launches with events")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(box, N, seconds: float):
+    """The oracle as it stands (plain numpy fp64, single thread) on a bounded sample of the
+    same workload: k CG iterations of the same box, k chosen to take ~`seconds`."""
+    import numpy as np
+    from oracle import basis, cg as ocg, forcing as of, mesh as om, operator as oo
+    from paper_2202_12477_b200 import ledger
+    x, w, D = basis.basis(N)
+    E, NG, NL = om.global_sizes(*box, N)
+    gid = om.l2g(*box, N)
+    G = om.geometric_factors(E, N, w)
+    W = om.weights_W(gid, NG)
+    b = of.forcing(range(NG), 1)
+    A = lambda v: oo.apply(v, gid, D, G, 1.0, W)
+    t0 = time.perf_counter()
+    ocg.cg(A, b, max_iters=1)
+    t1 = time.perf_counter() - t0
+    k = max(1, min(100, int(seconds / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    ocg.cg(A, b, max_iters=k)
+    t = time.perf_counter() - t0
+    gf = ledger.nekbone_flops_per_iter(E, N) * k / t / 1e9
+    return {"value": gf, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": f"{k} CG iterations (of 100) of box {box[0]}x{box[1]}x{box[2]} N={N}, numpy fp64, 1 thread",
+            "seconds": t, "iterations": k}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    box = tuple(int(v) for v in args.box.split(","))
+    N = args.N
+    import numpy as np
+    from oracle import basis, cg as ocg, forcing as of, mesh as om, operator as oo
+    from paper_2202_12477_b200 import ledger
+    x, w, D = basis.basis(N)
+    E, NG, NL = om.global_sizes(*box, N)
+    gid = om.l2g(*box, N)
+    G = om.geometric_factors(E, N, w)
+    W = om.weights_W(gid, NG)
+    b = of.forcing(range(NG), 1)
+    A = lambda v: oo.apply(v, gid, D, G, 1.0, W)
+    # each step: a bounded sample of the 100-iteration solve (sized so the run ends in minutes)
+    t0 = time.perf_counter()
+    ocg.cg(A, b, max_iters=1)
+    t1 = time.perf_counter() - t0
+    k = max(1, min(args.iters, int(8.0 / max(t1, 1e-6))))
+    for _ in range(args.warmup):
+        ocg.cg(A, b, max_iters=1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ocg.cg(A, b, max_iters=k)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    gf = ledger.nekbone_flops_per_iter(E, N) * k / t / 1e9
+    sample = f"{k} CG iterations per step (of {args.iters}) of box {box[0]}x{box[1]}x{box[2]} N={N}"
+    out = {"impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"C2: N={N}, E={box[0]}x{box[1]}x{box[2]}, {args.iters} CG iterations (sampled)",
+                      "box": list(box), "N": N, "N_G": NG, "lambda": 1.0},
+           "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2202_12477_b200 as hb
+    from paper_2202_12477_b200 import ledger
+
+    blk = tuple(int(v) for v in args.box.split(","))
+    N = args.N
+    comm = None
+    if world > 1:
+        grid = hb.rank_grid(world, 64, 64, 64)  # rank grid shape only (px >= py >= pz)
+        box = (blk[0] * grid[0], blk[1] * grid[1], blk[2] * grid[2])
+        uid = [hb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = hb.Comm(world, rank, uid[0])
+        mesh = hb.Mesh(*box, N, P=world, rank=rank, grid=grid)
+    else:
+        box = blk
+        mesh = hb.Mesh(*box, N)
+    op = hb.Operator(mesh, lam=1.0, comm=comm)
+    s = mesh.sizes
+    n = op.n_owned
+    E_glob, NG = s["E_global"], s["N_G"]
+    NL_loc, NG_loc_ref = s["N_L"], n
+    K = args.iters
+    stream = torch.cuda.current_stream()
+    b = torch.empty(n, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(b)
+    op.forcing(1, b)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
+
+    def step():
+        op.cg(b, x, K)
+
+    if not args.no_profile:
+        op.set_profiling(True)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region: K steps, device-timed with events, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    op_times = []
+    l0 = op.launch_count()
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for t in range(args.steps):
+            flush.zero_()
+            ev[t][0].record(stream)
+            step()
+            ev[t][1].record(stream)
+            if not args.no_profile:
+                op_times.append(op.kernel_time())  # synchronises on this step's last op event
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = op.launch_count() - l0
+    step_ms = [a.elapsed_time(bv) for a, bv in ev]
+    my_ms = sum(step_ms) / len(step_ms)
+    tmax = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = tmax.item()
+    fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (ms * 1e-3) / 1e9
+    gdofs = NG * K / (ms * 1e-3) / 1e9
+
+    # ---- end-to-end: same solve through the host-buffer C-ABI call (H2D + D2H inside)
+    bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b.cpu())
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    bnp, xnp = bh.numpy(), xh.numpy()
+    op.set_profiling(False)
+    for _ in range(2):
+        op.cg_host(bnp, xnp, K, hist=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = []
+    for t in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op.cg_host(bnp, xnp, K, hist=False)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (e2e_t.item() * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (operator), from the live event timings
+    peak, peak_src = peaks()
+    roof = None
+    if op_times:
+        n_l = sum(c for c, _ in op_times)
+        mean_s = sum(c * t for c, t in op_times) / max(n_l, 1)
+        alg_bytes = ledger.op_bytes_fused(n, NL_loc, 0)
+        achieved = alg_bytes / mean_s / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_op_summary.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                pj = json.load(f)
+            key = f"N{N}_{blk[0]}x{blk[1]}x{blk[2]}"
+            traffic = pj.get("dram_bytes_per_launch", {}).get(key)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": f"ax_layered<N={N}>", "launch_ms": round(mean_s * 1e3, 4), "launches_timed": n_l,
+                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "paper_ledger_gbs": round(ledger.op_bytes_paper(n, NL_loc) / mean_s / 1e9, 1),
+                "op_gflops": round(ledger.op_flops(s["E_local"], N) / mean_s / 1e9, 1)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(box, N, args.cpu_seconds)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(fom, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+               "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": f"C2: N={N}, E={box[0]}x{box[1]}x{box[2]} box, {K} CG iterations per step"
+                                      + (f" (C4-shaped weak scaling, {blk[0]}x{blk[1]}x{blk[2]} per GPU)" if world > 1 else ""),
+                          "box": list(box), "N": N, "E": E_glob, "N_G": NG, "N_L": E_glob * (N + 1) ** 3,
+                          "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
+                          "l2": "flushed between steps (256 MiB write); working set > L2",
+                          "parallelism": f"element partition p{world}"},
+               "gdofs_per_s": round(gdofs, 4),
+               "cg_bytes_per_iter_fused": ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3),
+               "cg_gbs_fused_ledger": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) * K / (ms * 1e-3) / 1e9, 1),
+               "e2e": {"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
+                       "d2h_bytes_per_step": 8 * n + 48},
+               "gpu_launches": launches,
+               "roofline": roof,
+               "cpu_baseline": cpu,
+               "clocks": clk.summary()}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

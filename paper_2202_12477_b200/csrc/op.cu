@@ -1,0 +1,900 @@
+// Device side of the C ABI: operator (hb_op_*), CG solve, forcing, dots, NCCL comm,
+// loopback groups and the 8:1 streaming calibration.  See include/hipbone_b200.h.
+//
+// Operator apply schedule (Fig. operator_timeline), P > 1:
+//   compute: init y | pack x at shared DOFs            comm: (wait) halo exchange -> xh
+//   compute: interior A  (overlaps the halo exchange)
+//   compute: (wait halo) halo elements -> y, yh        comm: (wait) assembly exchange yh -> recv
+//   compute: interior B  (overlaps the assembly exchange)
+//   compute: (wait assembly) y[send_loc] += recv
+// P = 1 is one kernel over all elements (plus the lambda-x init, folded into the CG p-update).
+// CG: per iteration  op(p) -> dot p.Ap [allreduce] -> x,r update + r.r [allreduce]
+// -> p update (writes the next assembly init lambda*p).  No host synchronisation inside the
+// loop; fixed-iteration mode is captured once into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <tuple>
+#include <vector>
+
+#include "ax_layered.cuh"
+#include "internal.h"
+#include "vec.cuh"
+
+using hb::set_error;
+
+#define CU_TRY(expr)                                                                      \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      set_error(std::string(__func__) + ": " #expr ": " + cudaGetErrorString(_e));        \
+      return (_e == cudaErrorMemoryAllocation) ? HB_ERR_OOM : HB_ERR_CUDA;                \
+    }                                                                                     \
+  } while (0)
+
+#define NC_TRY(expr)                                                                      \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess) {                                                              \
+      set_error(std::string(__func__) + ": " #expr ": " + ncclGetErrorString(_r));        \
+      return HB_ERR_NCCL;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+#define HB_TRY(expr)             \
+  do {                           \
+    int _s = (expr);             \
+    if (_s != HB_OK) return _s;  \
+  } while (0)
+
+struct hb_comm {
+  ncclComm_t nccl = nullptr;
+  int P = 1, rank = 0;
+};
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  int alloc(size_t b) {
+    if (p) { cudaFree(p); p = nullptr; }
+    bytes = b;
+    if (b == 0) return HB_OK;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) { p = nullptr; set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e)); return HB_ERR_OOM; }
+    return HB_OK;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct AxKernel {
+  const void* fn = nullptr;
+  int block = 0, epb = 0, grid_max = 0;
+  size_t smem = 0;
+};
+
+template <int N, bool HALO, bool MASSB>
+AxKernel make_ax() {
+  AxKernel k;
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_layered<N, HALO, MASSB>);
+  k.block = hbk::AxShape<N>::BLOCK;
+  k.epb = hbk::AxShape<N>::EPB;
+  k.smem = hbk::AxShape<N>::SMEM;
+  return k;
+}
+
+template <int N>
+AxKernel pick_ax_n(bool halo, bool massb) {
+  if (halo) return massb ? make_ax<N, true, true>() : make_ax<N, true, false>();
+  return massb ? make_ax<N, false, true>() : make_ax<N, false, false>();
+}
+
+AxKernel pick_ax(int N, bool halo, bool massb) {
+  switch (N) {
+    case 1: return pick_ax_n<1>(halo, massb);
+    case 2: return pick_ax_n<2>(halo, massb);
+    case 3: return pick_ax_n<3>(halo, massb);
+    case 4: return pick_ax_n<4>(halo, massb);
+    case 5: return pick_ax_n<5>(halo, massb);
+    case 6: return pick_ax_n<6>(halo, massb);
+    case 7: return pick_ax_n<7>(halo, massb);
+    case 8: return pick_ax_n<8>(halo, massb);
+    case 9: return pick_ax_n<9>(halo, massb);
+    case 10: return pick_ax_n<10>(halo, massb);
+    case 11: return pick_ax_n<11>(halo, massb);
+    case 12: return pick_ax_n<12>(halo, massb);
+    case 13: return pick_ax_n<13>(halo, massb);
+    case 14: return pick_ax_n<14>(halo, massb);
+    default: return pick_ax_n<15>(halo, massb);
+  }
+}
+
+// packed host G [E][NP3][6] -> device layout [E][NP][6][NP2]
+__global__ void relayout_G(const double* __restrict__ src, double* __restrict__ dst, int64_t E, int NP) {
+  const int NP2 = NP * NP, NP3 = NP2 * NP;
+  const int64_t total = E * NP3;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = s / NP3;
+    int n = (int)(s - e * NP3);
+    int k = n / NP2, c = n - k * NP2;
+    for (int f = 0; f < 6; ++f) dst[((e * NP + k) * 6 + f) * NP2 + c] = src[s * 6 + f];
+  }
+}
+
+// default box geometry written directly in device layout
+__global__ void box_G(double* __restrict__ dst, int64_t E, int N, double grr, double gss, double gtt) {
+  const int NP = N + 1, NP2 = NP * NP, NP3 = NP2 * NP;
+  const int64_t total = E * NP3;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = s / NP3;
+    int n = (int)(s - e * NP3);
+    int k = n / NP2, c = n - k * NP2;
+    int i = c % NP, j = c / NP;
+    double wq = hbk::c_D[0][i] * hbk::c_D[0][j] * hbk::c_D[0][k];  // weights staged in c_D[0]
+    double* d = dst + ((e * NP + k) * 6) * NP2 + c;
+    d[0] = wq * grr; d[NP2] = 0.0; d[2 * NP2] = 0.0;
+    d[3 * NP2] = wq * gss; d[4 * NP2] = 0.0; d[5 * NP2] = wq * gtt;
+  }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+int vec_grid(int64_t n) {
+  int64_t need = (n / 2 + hbk::VEC_BLOCK - 1) / hbk::VEC_BLOCK;
+  int64_t cap = (int64_t)num_sms() * 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
+}
+
+}  // namespace
+
+struct hb_op {
+  hb_sizes sz{};
+  int N = 0, NP3 = 0;
+  int mass_mode = 0;
+  double lam = 1.0;
+  hb_comm* comm = nullptr;
+  bool grouped = false;
+  int64_t nA = 0, nH = 0, nB = 0;
+  // device data
+  DevBuf idx, G, B, owned_gid;
+  DevBuf r, p, Ap, xs, partials, scal, hist, dot_out, dot_ticket;
+  DevBuf xh, yh, send_loc, send_buf, recv_buf;
+  std::vector<int32_t> nbr;
+  std::vector<int64_t> soff, scnt, roff, rcnt;
+  int64_t n_send = 0;
+  AxKernel ax_plain, ax_halo;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_haloel = nullptr, ev_gather = nullptr;
+  cudaEvent_t ev_red = nullptr, ev_red_done = nullptr;
+  // profiling
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
+  int64_t launches = 0;
+  // fixed-mode graph cache
+  struct GraphKey {
+    int32_t K; const double* b; double* x; bool prof; cudaStream_t st;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(K, b, x, prof, st) < std::tie(o.K, o.b, o.x, o.prof, o.st);
+    }
+  };
+  struct GraphVal { cudaGraphExec_t exec; int64_t launches; size_t prof_events; };
+  std::map<GraphKey, GraphVal> graphs;
+  double* host_scal = nullptr;  // pinned CgScalars mirror
+  ~hb_op() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& pr : prof_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    for (cudaEvent_t e : {ev_pack, ev_halo, ev_haloel, ev_gather, ev_red, ev_red_done}) if (e) cudaEventDestroy(e);
+    if (host_scal) cudaFreeHost(host_scal);
+  }
+};
+
+namespace {
+
+int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double* x, double* y, cudaStream_t st) {
+  if (e1 <= e0) return HB_OK;
+  hbk::AxArgs a;
+  a.idx = op->idx.as<int32_t>();
+  a.G = op->G.as<double>();
+  a.B = op->B.as<double>();
+  a.x = x;
+  a.xh = op->xh.as<double>();
+  a.y = y;
+  a.yh = op->yh.as<double>();
+  a.e_begin = e0; a.e_end = e1;
+  a.n_owned = (int32_t)op->sz.n_owned;
+  a.lam = op->lam;
+  int64_t groups = (e1 - e0 + k.epb - 1) / k.epb;
+  int grid = (int)std::min<int64_t>(groups, (int64_t)k.grid_max);
+  void* args[] = {&a};
+  cudaEvent_t e_start = nullptr, e_stop = nullptr;
+  if (op->profiling) {
+    if (op->prof_used >= op->prof_events.size()) {
+      cudaEvent_t s0, s1;
+      CU_TRY(cudaEventCreate(&s0));
+      CU_TRY(cudaEventCreate(&s1));
+      op->prof_events.push_back({s0, s1});
+    }
+    e_start = op->prof_events[op->prof_used].first;
+    e_stop = op->prof_events[op->prof_used].second;
+    op->prof_used++;
+    CU_TRY(cudaEventRecordWithFlags(e_start, st, cudaEventRecordExternal));
+  }
+  CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
+  op->launches++;
+  if (op->profiling) CU_TRY(cudaEventRecordWithFlags(e_stop, st, cudaEventRecordExternal));
+  return HB_OK;
+}
+
+int allreduce_sum(hb_op* op, double* v, cudaStream_t st) {
+  if (!op->comm || op->comm->P == 1) return HB_OK;
+  NC_TRY(ncclAllReduce(v, v, 1, ncclFloat64, ncclSum, op->comm->nccl, st));
+  return HB_OK;
+}
+
+// --- staged apply (shared by the single-op path and loopback groups)
+int stage_init(hb_op* op, const double* x, double* y, bool init_y, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  if (init_y) {
+    hbk::vec_scale<<<vec_grid(2 * n), hbk::VEC_BLOCK, 0, st>>>(x, y, n, op->mass_mode == 0 ? op->lam : 0.0);
+    op->launches++;
+  }
+  if (op->sz.n_halo > 0) CU_TRY(cudaMemsetAsync(op->yh.p, 0, op->sz.n_halo * 8, st));
+  if (op->n_send > 0) {
+    hbk::pack_kernel<<<vec_grid(2 * op->n_send), hbk::VEC_BLOCK, 0, st>>>(x, op->send_loc.as<int32_t>(),
+                                                                       op->send_buf.as<double>(), op->n_send);
+    op->launches++;
+  }
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+int stage_unpack(hb_op* op, double* y, cudaStream_t st) {
+  if (op->n_send > 0) {
+    hbk::unpack_add_kernel<<<vec_grid(2 * op->n_send), hbk::VEC_BLOCK, 0, st>>>(y, op->send_loc.as<int32_t>(),
+                                                                             op->recv_buf.as<double>(), op->n_send);
+    op->launches++;
+  }
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+int nccl_halo_exchange(hb_op* op, cudaStream_t cs) {
+  NC_TRY(ncclGroupStart());
+  for (size_t q = 0; q < op->nbr.size(); ++q) {
+    if (op->scnt[q]) NC_TRY(ncclSend(op->send_buf.as<double>() + op->soff[q], op->scnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
+    if (op->rcnt[q]) NC_TRY(ncclRecv(op->xh.as<double>() + op->roff[q], op->rcnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
+  }
+  NC_TRY(ncclGroupEnd());
+  return HB_OK;
+}
+
+int nccl_assembly_exchange(hb_op* op, cudaStream_t cs) {
+  NC_TRY(ncclGroupStart());
+  for (size_t q = 0; q < op->nbr.size(); ++q) {
+    if (op->rcnt[q]) NC_TRY(ncclSend(op->yh.as<double>() + op->roff[q], op->rcnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
+    if (op->scnt[q]) NC_TRY(ncclRecv(op->recv_buf.as<double>() + op->soff[q], op->scnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
+  }
+  NC_TRY(ncclGroupEnd());
+  return HB_OK;
+}
+
+// y = A x for one op (P = 1, or P > 1 with NCCL).  init_y=false: y already holds the
+// assembly initialisation (lambda x or 0), as written by the CG p-update.
+int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStream_t st) {
+  const int64_t E = op->sz.E_local;
+  const bool multi = op->comm && op->comm->P > 1;
+  if (!multi) {
+    HB_TRY(stage_init(op, x, y, init_y, st));
+    return launch_ax(op, op->ax_plain, 0, E, x, y, st);
+  }
+  cudaStream_t cs = op->comm_stream;
+  HB_TRY(stage_init(op, x, y, init_y, st));
+  CU_TRY(cudaEventRecord(op->ev_pack, st));
+  CU_TRY(cudaStreamWaitEvent(cs, op->ev_pack, 0));
+  HB_TRY(nccl_halo_exchange(op, cs));
+  CU_TRY(cudaEventRecord(op->ev_halo, cs));
+  HB_TRY(launch_ax(op, op->ax_plain, 0, op->nA, x, y, st));                          // interior A
+  CU_TRY(cudaStreamWaitEvent(st, op->ev_halo, 0));
+  HB_TRY(launch_ax(op, op->ax_halo, op->nA, op->nA + op->nH, x, y, st));             // halo elements
+  CU_TRY(cudaEventRecord(op->ev_haloel, st));
+  CU_TRY(cudaStreamWaitEvent(cs, op->ev_haloel, 0));
+  HB_TRY(nccl_assembly_exchange(op, cs));
+  CU_TRY(cudaEventRecord(op->ev_gather, cs));
+  HB_TRY(launch_ax(op, op->ax_plain, op->nA + op->nH, E, x, y, st));                 // interior B
+  CU_TRY(cudaStreamWaitEvent(st, op->ev_gather, 0));
+  return stage_unpack(op, y, st);
+}
+
+}  // namespace
+
+extern "C" int hb_comm_unique_id(uint8_t id[128]) {
+  if (!id) { set_error("hb_comm_unique_id: null pointer"); return HB_ERR_ARG; }
+  ncclUniqueId u;
+  NC_TRY(ncclGetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return HB_OK;
+}
+
+extern "C" int hb_comm_create(int P, int rank, const uint8_t id[128], hb_comm** out) {
+  if (!id || !out || P < 1 || rank < 0 || rank >= P) { set_error("hb_comm_create: bad argument"); return HB_ERR_ARG; }
+  *out = nullptr;
+  auto* c = new (std::nothrow) hb_comm();
+  if (!c) { set_error("hb_comm_create: out of memory"); return HB_ERR_OOM; }
+  c->P = P; c->rank = rank;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, P, u, rank);
+  if (r != ncclSuccess) { set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); delete c; return HB_ERR_NCCL; }
+  *out = c;
+  return HB_OK;
+}
+
+extern "C" int hb_comm_destroy(hb_comm* c) {
+  if (!c) return HB_OK;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return HB_OK;
+}
+
+static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaStream_t st, hb_op* op) {
+  HB_TRY(hb_mesh_sizes(m, &op->sz));
+  op->N = m->box.N; op->NP3 = m->NP3;
+  op->mass_mode = m->box.mass_mode;
+  op->lam = lambda;
+  op->comm = comm;
+  op->nA = m->nA; op->nH = m->nH; op->nB = m->nB;
+  const int N = op->N, NP = N + 1, NP3 = m->NP3;
+  const int64_t E = op->sz.E_local, NL = E * NP3, n = op->sz.n_owned;
+  // constant D for this N (and the GLL weights in row 0 for the box geometry kernel)
+  {
+    double Dp[256] = {0};
+    for (int t = 0; t < NP * NP; ++t) Dp[t] = m->D[t];
+    CU_TRY(cudaMemcpyToSymbol(hbk::c_D, Dp, sizeof(Dp), sizeof(double) * 256 * N));
+  }
+  HB_TRY(op->idx.alloc(NL * sizeof(int32_t)));
+  CU_TRY(cudaMemcpyAsync(op->idx.p, m->idx.data(), NL * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  HB_TRY(op->G.alloc(NL * 6 * sizeof(double)));
+  if (m->has_G) {
+    DevBuf tmp;
+    HB_TRY(tmp.alloc(NL * 6 * sizeof(double)));
+    CU_TRY(cudaMemcpyAsync(tmp.p, m->G_custom.data(), NL * 6 * sizeof(double), cudaMemcpyHostToDevice, st));
+    relayout_G<<<num_sms() * 8, 256, 0, st>>>(tmp.as<double>(), op->G.as<double>(), E, NP);
+    CU_TRY(cudaGetLastError());
+    CU_TRY(cudaStreamSynchronize(st));
+  } else if (NL > 0) {
+    double wrow[256] = {0};
+    for (int t = 0; t < NP; ++t) wrow[t] = m->w[t];
+    CU_TRY(cudaMemcpyToSymbol(hbk::c_D, wrow, sizeof(wrow), 0));
+    const double hx = m->box.ext[0], hy = m->box.ext[1], hz = m->box.ext[2];
+    const double J = hx * hy * hz / 8.0;
+    box_G<<<num_sms() * 8, 256, 0, st>>>(op->G.as<double>(), E, N, J * 4.0 / (hx * hx), J * 4.0 / (hy * hy), J * 4.0 / (hz * hz));
+    CU_TRY(cudaGetLastError());
+  }
+  if (op->mass_mode == 1) {
+    std::vector<double> Bh(NL);
+    HB_TRY(hb_mesh_mass(m, Bh.data()));
+    HB_TRY(op->B.alloc(NL * sizeof(double)));
+    CU_TRY(cudaMemcpyAsync(op->B.p, Bh.data(), NL * sizeof(double), cudaMemcpyHostToDevice, st));
+    CU_TRY(cudaStreamSynchronize(st));
+  }
+  if (m->P > 1) {
+    HB_TRY(op->owned_gid.alloc(n * sizeof(int64_t)));
+    CU_TRY(cudaMemcpyAsync(op->owned_gid.p, m->owned.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
+  // CG workspace
+  HB_TRY(op->r.alloc(std::max<int64_t>(n, 1) * 8));
+  HB_TRY(op->p.alloc(std::max<int64_t>(n, 1) * 8));
+  HB_TRY(op->Ap.alloc(std::max<int64_t>(n, 1) * 8));
+  HB_TRY(op->xs.alloc(std::max<int64_t>(n, 1) * 8));
+  HB_TRY(op->partials.alloc((size_t)num_sms() * 8 * 8 + 64));
+  HB_TRY(op->scal.alloc(sizeof(hbk::CgScalars)));
+  CU_TRY(cudaMemsetAsync(op->scal.p, 0, sizeof(hbk::CgScalars), st));
+  HB_TRY(op->dot_out.alloc(8));
+  HB_TRY(op->dot_ticket.alloc(8));
+  CU_TRY(cudaMemsetAsync(op->dot_ticket.p, 0, 8, st));
+  CU_TRY(cudaMallocHost(&op->host_scal, sizeof(hbk::CgScalars)));
+  // halo / exchange plans
+  const int64_t nh = op->sz.n_halo;
+  HB_TRY(op->xh.alloc(nh * 8));
+  HB_TRY(op->yh.alloc(nh * 8));
+  op->nbr = m->nbr;
+  const size_t nn = m->nbr.size();
+  op->soff.assign(nn, 0); op->scnt.assign(nn, 0); op->roff = m->recv_off; op->rcnt = m->recv_cnt;
+  std::vector<int32_t> sl;
+  for (size_t q = 0; q < nn; ++q) {
+    op->soff[q] = (int64_t)sl.size();
+    op->scnt[q] = (int64_t)m->send_loc[q].size();
+    sl.insert(sl.end(), m->send_loc[q].begin(), m->send_loc[q].end());
+  }
+  op->n_send = (int64_t)sl.size();
+  HB_TRY(op->send_loc.alloc(sl.size() * 4));
+  HB_TRY(op->send_buf.alloc(sl.size() * 8));
+  HB_TRY(op->recv_buf.alloc(sl.size() * 8));
+  if (!sl.empty()) CU_TRY(cudaMemcpyAsync(op->send_loc.p, sl.data(), sl.size() * 4, cudaMemcpyHostToDevice, st));
+  // kernels
+  op->ax_plain = pick_ax(N, false, op->mass_mode == 1);
+  op->ax_halo = pick_ax(N, true, op->mass_mode == 1);
+  for (AxKernel* k : {&op->ax_plain, &op->ax_halo}) {
+    int nb = 0;
+    CU_TRY(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
+    CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k->fn, k->block, k->smem));
+    k->grid_max = std::max(1, nb) * num_sms();
+  }
+  if (m->P > 1 && comm) {
+    int lo, hi;
+    CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU_TRY(cudaStreamCreateWithPriority(&op->comm_stream, cudaStreamNonBlocking, hi));
+  }
+  for (cudaEvent_t* e : {&op->ev_pack, &op->ev_halo, &op->ev_haloel, &op->ev_gather, &op->ev_red, &op->ev_red_done})
+    CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  CU_TRY(cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+extern "C" int hb_op_create(const hb_mesh* m, hb_comm* comm, double lambda, void* stream, hb_op** out) {
+  if (!m || !out) { set_error("hb_op_create: null pointer"); return HB_ERR_ARG; }
+  *out = nullptr;
+  if (m->P > 1 && comm && (comm->P != m->P || comm->rank != m->rank)) {
+    set_error("hb_op_create: comm (P, rank) does not match the mesh"); return HB_ERR_STATE;
+  }
+  if (m->P == 1 && comm && comm->P != 1) { set_error("hb_op_create: comm given for a P=1 mesh"); return HB_ERR_STATE; }
+  auto* op = new (std::nothrow) hb_op();
+  if (!op) { set_error("hb_op_create: out of memory"); return HB_ERR_OOM; }
+  int st = op_create_impl(m, comm, lambda, (cudaStream_t)stream, op);
+  if (st != HB_OK) { delete op; return st; }
+  *out = op;
+  return HB_OK;
+}
+
+static int check_multi(hb_op* op, const char* fn) {
+  if (op->sz.P > 1 && !op->comm) {
+    set_error(std::string(fn) + ": P>1 op without a communicator (use a loopback group)");
+    return HB_ERR_STATE;
+  }
+  return HB_OK;
+}
+
+extern "C" int hb_op_apply(hb_op* op, const double* x, double* y, void* stream) {
+  if (!op || (op->sz.n_owned > 0 && (!x || !y))) { set_error("hb_op_apply: null pointer"); return HB_ERR_ARG; }
+  if (x == y) { set_error("hb_op_apply: x and y must be distinct buffers"); return HB_ERR_ARG; }
+  HB_TRY(check_multi(op, "hb_op_apply"));
+  return apply_internal(op, x, y, true, (cudaStream_t)stream);
+}
+
+extern "C" int hb_forcing(hb_op* op, uint64_t seed, double* b, void* stream) {
+  if (!op || (op->sz.n_owned > 0 && !b)) { set_error("hb_forcing: null pointer"); return HB_ERR_ARG; }
+  const int64_t n = op->sz.n_owned;
+  if (n == 0) return HB_OK;
+  hbk::forcing_kernel<<<vec_grid(2 * n), hbk::VEC_BLOCK, 0, (cudaStream_t)stream>>>(b, op->owned_gid.as<int64_t>(), n, seed);
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+static int local_dot(hb_op* op, const double* a, const double* b, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  hbk::vec_dot<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(a, b, n, op->partials.as<double>(),
+                                                                               op->dot_ticket.as<uint32_t>(), op->dot_out.as<double>());
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+extern "C" int hb_dot(hb_op* op, const double* a, const double* b, double* out_host, void* stream) {
+  if (!op || !out_host || (op->sz.n_owned > 0 && (!a || !b))) { set_error("hb_dot: null pointer"); return HB_ERR_ARG; }
+  HB_TRY(check_multi(op, "hb_dot"));
+  cudaStream_t st = (cudaStream_t)stream;
+  HB_TRY(local_dot(op, a, b, st));
+  HB_TRY(allreduce_sum(op, op->dot_out.as<double>(), st));
+  CU_TRY(cudaMemcpyAsync(out_host, op->dot_out.p, 8, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+namespace {
+
+double lam_init(const hb_op* op) { return op->mass_mode == 0 ? op->lam : 0.0; }
+
+int cg_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  hbk::cg_init<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+      b, x, op->r.as<double>(), op->p.as<double>(), op->Ap.as<double>(), n, lam_init(op),
+      op->partials.as<double>(), op->scal.as<hbk::CgScalars>());
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
+  return allreduce_sum(op, &s->rr_new, st);
+}
+
+// One CG iteration after the operator: dot, x/r update, optionally the p update.
+int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
+  const int gv = vec_grid(std::max<int64_t>(n, 1));
+  hbk::cg_dot_pAp<<<gv, hbk::VEC_BLOCK, 0, st>>>(op->p.as<double>(), op->Ap.as<double>(), n,
+                                                 op->partials.as<double>(), s, op->hist.as<double>());
+  op->launches++;
+  HB_TRY(allreduce_sum(op, &s->pAp, st));
+  hbk::cg_update_xr<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n,
+                                                   op->partials.as<double>(), s);
+  op->launches++;
+  HB_TRY(allreduce_sum(op, &s->rr_new, st));
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+int cg_vec_part2(hb_op* op, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  hbk::cg_update_p<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+      op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n, lam_init(op), op->scal.as<hbk::CgScalars>());
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+int cg_iteration(hb_op* op, double* x, cudaStream_t st) {
+  HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st));
+  HB_TRY(cg_vec_part1(op, x, st));
+  return cg_vec_part2(op, st);
+}
+
+int ensure_hist(hb_op* op, int32_t K) {
+  size_t need = (size_t)(K + 1) * 8;
+  if (op->hist.bytes < need) {
+    // graphs reference the old history buffer
+    for (auto& kv : op->graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->graphs.clear();
+    HB_TRY(op->hist.alloc(need));
+  }
+  return HB_OK;
+}
+
+int finish_result(hb_op* op, int32_t iters, double* rr_hist_host, hb_cg_result* res, cudaStream_t st) {
+  CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+  if (rr_hist_host && iters > 0)
+    CU_TRY(cudaMemcpyAsync(rr_hist_host, op->hist.p, (size_t)iters * 8, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  const hbk::CgScalars* hs = reinterpret_cast<const hbk::CgScalars*>(op->host_scal);
+  if (rr_hist_host) rr_hist_host[iters] = hs->rr_new;
+  if (res) {
+    res->iterations = iters;
+    res->rr_final = hs->rr_new;
+    res->rr0 = rr_hist_host ? rr_hist_host[0] : (iters == 0 ? hs->rr_new : NAN);
+  }
+  return HB_OK;
+}
+
+int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_host, hb_cg_result* res,
+             cudaStream_t st) {
+  HB_TRY(ensure_hist(op, K));
+  hb_op::GraphKey key{K, b, x, op->profiling, st};
+  auto it = op->graphs.find(key);
+  if (op->profiling) op->prof_used = 0;  // a profiling graph records into events 0..n-1
+  if (it == op->graphs.end()) {
+    int64_t l0 = op->launches;
+    cudaGraph_t graph;
+    CU_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    int status = cg_init(op, b, x, st);
+    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, st);
+    cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
+    CU_TRY(ce);
+    cudaGraphExec_t exec;
+    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CU_TRY(ie);
+    it = op->graphs.emplace(key, hb_op::GraphVal{exec, op->launches - l0, op->prof_used}).first;
+    op->launches = l0;
+  }
+  op->prof_used = it->second.prof_events;
+  CU_TRY(cudaGraphLaunch(it->second.exec, st));
+  op->launches += it->second.launches;
+  return finish_result(op, K, rr_hist_host, res, st);
+}
+
+int cg_tol(hb_op* op, const double* b, double* x, int32_t max_iters, double eps, double* rr_hist_host,
+           hb_cg_result* res, cudaStream_t st) {
+  HB_TRY(ensure_hist(op, max_iters));
+  hbk::CgScalars* hs = reinterpret_cast<hbk::CgScalars*>(op->host_scal);
+  HB_TRY(cg_init(op, b, x, st));
+  CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  int32_t j = 0;
+  double rr = hs->rr_new;
+  while (j < max_iters && rr > eps) {
+    HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st));
+    HB_TRY(cg_vec_part1(op, x, st));
+    CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_new)) {
+      set_error("hb_cg_solve: breakdown (p.Ap <= 0 or non-finite) at iteration " + std::to_string(j));
+      return HB_ERR_BREAKDOWN;
+    }
+    HB_TRY(cg_vec_part2(op, st));
+    ++j;
+    rr = hs->rr_new;
+  }
+  return finish_result(op, j, rr_hist_host, res, st);
+}
+
+}  // namespace
+
+extern "C" int hb_cg_solve(hb_op* op, const double* b, double* x, int32_t max_iters, double eps,
+                           double* rr_hist_host, hb_cg_result* res, void* stream) {
+  if (!op || (op->sz.n_owned > 0 && (!b || !x))) { set_error("hb_cg_solve: null pointer"); return HB_ERR_ARG; }
+  if (max_iters < 0) { set_error("hb_cg_solve: max_iters must be >= 0"); return HB_ERR_ARG; }
+  HB_TRY(check_multi(op, "hb_cg_solve"));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (eps < 0) return cg_fixed(op, b, x, max_iters, rr_hist_host, res, st);
+  return cg_tol(op, b, x, max_iters, eps, rr_hist_host, res, st);
+}
+
+extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t max_iters, double eps,
+                                double* rr_hist_host, hb_cg_result* res, void* stream) {
+  if (!op || (op->sz.n_owned > 0 && (!b_host || !x_host))) { set_error("hb_cg_solve_host: null pointer"); return HB_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)op->sz.n_owned * 8;
+  // b is staged through the internal x buffer's twin: use r as the device copy of b
+  // (cg_init reads b before writing r, element by element, so aliasing is safe).
+  double* b_dev = op->r.as<double>();
+  if (bytes) CU_TRY(cudaMemcpyAsync(b_dev, b_host, bytes, cudaMemcpyHostToDevice, st));
+  HB_TRY(hb_cg_solve(op, b_dev, op->xs.as<double>(), max_iters, eps, rr_hist_host, res, stream));
+  if (bytes) CU_TRY(cudaMemcpyAsync(x_host, op->xs.p, bytes, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+extern "C" int hb_op_set_profiling(hb_op* op, int enable) {
+  if (!op) { set_error("hb_op_set_profiling: null pointer"); return HB_ERR_ARG; }
+  if ((bool)enable != op->profiling) {
+    op->profiling = enable != 0;
+  }
+  op->prof_used = 0;
+  return HB_OK;
+}
+
+extern "C" int hb_op_kernel_time(hb_op* op, int64_t* launches, double* mean_seconds) {
+  if (!op || !launches || !mean_seconds) { set_error("hb_op_kernel_time: null pointer"); return HB_ERR_ARG; }
+  double tot = 0.0;
+  for (size_t t = 0; t < op->prof_used; ++t) {
+    float ms = 0.f;
+    CU_TRY(cudaEventSynchronize(op->prof_events[t].second));
+    CU_TRY(cudaEventElapsedTime(&ms, op->prof_events[t].first, op->prof_events[t].second));
+    tot += ms * 1e-3;
+  }
+  *launches = (int64_t)op->prof_used;
+  *mean_seconds = op->prof_used ? tot / op->prof_used : 0.0;
+  return HB_OK;
+}
+
+extern "C" int hb_op_launch_count(hb_op* op, int64_t* launches) {
+  if (!op || !launches) { set_error("hb_op_launch_count: null pointer"); return HB_ERR_ARG; }
+  *launches = op->launches;
+  return HB_OK;
+}
+
+extern "C" int hb_op_sizes(const hb_op* op, hb_sizes* out) {
+  if (!op || !out) { set_error("hb_op_sizes: null pointer"); return HB_ERR_ARG; }
+  *out = op->sz;
+  return HB_OK;
+}
+
+extern "C" int hb_op_destroy(hb_op* op) {
+  if (op) cudaDeviceSynchronize();
+  delete op;
+  return HB_OK;
+}
+
+// ------------------------------------------------------------------ loopback groups
+struct hb_group {
+  std::vector<hb_op*> ops;
+  std::vector<std::vector<int>> peer_index;  // [rank][q] -> index of `rank` in nbr list of nbr[q]
+  DevBuf sums;                               // per-rank scalar staging
+};
+
+extern "C" int hb_group_create(hb_op* const* ops, int P, hb_group** out) {
+  if (!ops || !out || P < 1) { set_error("hb_group_create: bad argument"); return HB_ERR_ARG; }
+  *out = nullptr;
+  auto* g = new (std::nothrow) hb_group();
+  if (!g) { set_error("hb_group_create: out of memory"); return HB_ERR_OOM; }
+  for (int r = 0; r < P; ++r) {
+    if (!ops[r] || ops[r]->sz.P != P || ops[r]->sz.rank != r || ops[r]->comm) {
+      set_error("hb_group_create: ops must be the P comm-less ops of one partition, in rank order");
+      delete g; return HB_ERR_STATE;
+    }
+    g->ops.push_back(ops[r]);
+  }
+  g->peer_index.resize(P);
+  for (int r = 0; r < P; ++r) {
+    hb_op* a = g->ops[r];
+    for (size_t q = 0; q < a->nbr.size(); ++q) {
+      hb_op* b = g->ops[a->nbr[q]];
+      auto itq = std::find(b->nbr.begin(), b->nbr.end(), r);
+      if (itq == b->nbr.end()) { set_error("hb_group_create: asymmetric neighbour sets"); delete g; return HB_ERR_SETUP; }
+      int back = (int)(itq - b->nbr.begin());
+      if (a->scnt[q] != b->rcnt[back] || a->rcnt[q] != b->scnt[back]) {
+        set_error("hb_group_create: send/recv plan sizes disagree"); delete g; return HB_ERR_SETUP;
+      }
+      g->peer_index[r].push_back(back);
+    }
+    a->grouped = true;
+  }
+  int st = g->sums.alloc(8 * P);
+  if (st) { delete g; return st; }
+  *out = g;
+  return HB_OK;
+}
+
+namespace {
+// device-to-device "transport": what rank r sends to nbr[q] lands in that rank's buffer
+int group_halo_exchange(hb_group* g, cudaStream_t st) {
+  for (size_t r = 0; r < g->ops.size(); ++r) {
+    hb_op* a = g->ops[r];
+    for (size_t q = 0; q < a->nbr.size(); ++q) {
+      hb_op* b = g->ops[a->nbr[q]];
+      int back = g->peer_index[r][q];
+      if (a->scnt[q])
+        CU_TRY(cudaMemcpyAsync(b->xh.as<double>() + b->roff[back], a->send_buf.as<double>() + a->soff[q],
+                               a->scnt[q] * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  return HB_OK;
+}
+
+int group_assembly_exchange(hb_group* g, cudaStream_t st) {
+  for (size_t r = 0; r < g->ops.size(); ++r) {
+    hb_op* a = g->ops[r];
+    for (size_t q = 0; q < a->nbr.size(); ++q) {
+      hb_op* b = g->ops[a->nbr[q]];
+      int back = g->peer_index[r][q];
+      if (a->rcnt[q])
+        CU_TRY(cudaMemcpyAsync(b->recv_buf.as<double>() + b->soff[back], a->yh.as<double>() + a->roff[q],
+                               a->rcnt[q] * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  return HB_OK;
+}
+
+int group_apply_internal(hb_group* g, const double* const* x, double* const* y, bool init_y, cudaStream_t st) {
+  const size_t P = g->ops.size();
+  for (size_t r = 0; r < P; ++r) HB_TRY(stage_init(g->ops[r], x[r], y[r], init_y, st));
+  HB_TRY(group_halo_exchange(g, st));
+  for (size_t r = 0; r < P; ++r) HB_TRY(launch_ax(g->ops[r], g->ops[r]->ax_plain, 0, g->ops[r]->nA, x[r], y[r], st));
+  for (size_t r = 0; r < P; ++r) {
+    hb_op* a = g->ops[r];
+    HB_TRY(launch_ax(a, a->ax_halo, a->nA, a->nA + a->nH, x[r], y[r], st));
+  }
+  HB_TRY(group_assembly_exchange(g, st));
+  for (size_t r = 0; r < P; ++r) {
+    hb_op* a = g->ops[r];
+    HB_TRY(launch_ax(a, a->ax_plain, a->nA + a->nH, a->sz.E_local, x[r], y[r], st));
+  }
+  for (size_t r = 0; r < P; ++r) HB_TRY(stage_unpack(g->ops[r], y[r], st));
+  return HB_OK;
+}
+
+__global__ void group_sum_kernel(double* const* parts, int P, double* const* dsts) {
+  // every rank receives the rank-ordered sum of the P local values (allreduce stand-in)
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += *parts[r];
+  for (int r = 0; r < P; ++r) *dsts[r] = s;
+}
+
+int group_allreduce(hb_group* g, size_t field_offset, cudaStream_t st) {
+  const int P = (int)g->ops.size();
+  std::vector<double*> ptrs(P);
+  for (int r = 0; r < P; ++r) ptrs[r] = reinterpret_cast<double*>(g->ops[r]->scal.as<char>() + field_offset);
+  // stage the pointer table in the group's scratch (P doubles reinterpreted as pointers)
+  CU_TRY(cudaMemcpyAsync(g->sums.p, ptrs.data(), P * sizeof(double*), cudaMemcpyHostToDevice, st));
+  double* const* table = g->sums.as<double*>();
+  group_sum_kernel<<<1, 1, 0, st>>>(table, P, table);
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+}  // namespace
+
+extern "C" int hb_group_apply(hb_group* g, const double* const* x, double* const* y, void* stream) {
+  if (!g || !x || !y) { set_error("hb_group_apply: null pointer"); return HB_ERR_ARG; }
+  return group_apply_internal(g, x, y, true, (cudaStream_t)stream);
+}
+
+extern "C" int hb_group_cg_solve(hb_group* g, const double* const* b, double* const* x, int32_t max_iters, double eps,
+                                 double* rr_hist_host, hb_cg_result* res, void* stream) {
+  if (!g || !b || !x || max_iters < 0) { set_error("hb_group_cg_solve: bad argument"); return HB_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = (int)g->ops.size();
+  for (int r = 0; r < P; ++r) HB_TRY(ensure_hist(g->ops[r], max_iters));
+  const size_t off_pAp = offsetof(hbk::CgScalars, pAp), off_rrn = offsetof(hbk::CgScalars, rr_new);
+  for (int r = 0; r < P; ++r) HB_TRY(cg_init(g->ops[r], b[r], x[r], st));
+  HB_TRY(group_allreduce(g, off_rrn, st));
+  hb_op* o0 = g->ops[0];
+  hbk::CgScalars* hs = reinterpret_cast<hbk::CgScalars*>(o0->host_scal);
+  auto read0 = [&]() -> int {
+    CU_TRY(cudaMemcpyAsync(o0->host_scal, o0->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    return HB_OK;
+  };
+  HB_TRY(read0());
+  double rr = hs->rr_new;
+  int32_t j = 0;
+  std::vector<const double*> pv(P);
+  std::vector<double*> av(P);
+  for (int r = 0; r < P; ++r) { pv[r] = g->ops[r]->p.as<double>(); av[r] = g->ops[r]->Ap.as<double>(); }
+  while (j < max_iters && (eps < 0 || rr > eps)) {
+    HB_TRY(group_apply_internal(g, pv.data(), av.data(), false, st));
+    for (int r = 0; r < P; ++r) {
+      hb_op* a = g->ops[r];
+      const int64_t n = a->sz.n_owned;
+      hbk::cg_dot_pAp<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+          a->p.as<double>(), a->Ap.as<double>(), n, a->partials.as<double>(), a->scal.as<hbk::CgScalars>(), a->hist.as<double>());
+    }
+    HB_TRY(group_allreduce(g, off_pAp, st));
+    for (int r = 0; r < P; ++r) {
+      hb_op* a = g->ops[r];
+      const int64_t n = a->sz.n_owned;
+      hbk::cg_update_xr<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+          x[r], a->p.as<double>(), a->r.as<double>(), a->Ap.as<double>(), n, a->partials.as<double>(), a->scal.as<hbk::CgScalars>());
+    }
+    HB_TRY(group_allreduce(g, off_rrn, st));
+    if (eps >= 0) {
+      HB_TRY(read0());
+      if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_new)) {
+        set_error("hb_group_cg_solve: breakdown"); return HB_ERR_BREAKDOWN;
+      }
+      rr = hs->rr_new;
+    }
+    for (int r = 0; r < P; ++r) HB_TRY(cg_vec_part2(g->ops[r], st));
+    ++j;
+  }
+  return finish_result(o0, j, rr_hist_host, res, st);
+}
+
+extern "C" int hb_group_destroy(hb_group* g) {
+  if (g) for (hb_op* o : g->ops) o->grouped = false;
+  delete g;
+  return HB_OK;
+}
+
+// ------------------------------------------------------------------ 8:1 streaming calibration
+extern "C" int hb_stream_bench(int64_t n_out, int reps, double* bytes_per_s) {
+  if (n_out <= 0 || reps <= 0 || !bytes_per_s) { set_error("hb_stream_bench: bad argument"); return HB_ERR_ARG; }
+  DevBuf in, out;
+  HB_TRY(in.alloc((size_t)n_out * 8 * 8));
+  HB_TRY(out.alloc((size_t)n_out * 8));
+  CU_TRY(cudaMemset(in.p, 0, (size_t)n_out * 64));
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  const int grid = num_sms() * 8;
+  for (int w = 0; w < 3; ++w) hbk::stream8to1<<<grid, hbk::VEC_BLOCK>>>(in.as<double>(), out.as<double>(), n_out);
+  CU_TRY(cudaEventRecord(e0));
+  for (int t = 0; t < reps; ++t) hbk::stream8to1<<<grid, hbk::VEC_BLOCK>>>(in.as<double>(), out.as<double>(), n_out);
+  CU_TRY(cudaEventRecord(e1));
+  CU_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *bytes_per_s = 72.0 * (double)n_out * reps / (ms * 1e-3);
+  return HB_OK;
+}

@@ -1,0 +1,227 @@
+// CG vector kernels (K4 of SURVEY §2C): fused, vectorised, deterministic.
+//
+// Alg. 1 with the paper's fusions: p.Ap in its own reduction kernel;
+// r -= alpha Ap fused with r.r; x += alpha p; p = r + beta p.  alpha and beta never leave
+// the device: every kernel reads the reduced scalars from CgScalars and computes them
+// itself, so an iteration has no host round trip and can be captured in a CUDA graph.
+// Reductions: fp64 per thread -> warp shuffle -> CTA -> one partial per CTA; the last CTA
+// to finish (atomic ticket) sums the partials in CTA order, so results are deterministic
+// for a fixed grid.  With P > 1 the local sum is allreduced (NCCL) before use.
+#pragma once
+#include <cstdint>
+
+namespace hbk {
+
+struct CgScalars {
+  double pAp;      // p.Ap (global after allreduce)
+  double rr;       // r_j.r_j
+  double rr_new;   // r_{j+1}.r_{j+1} (global after allreduce)
+  double pad;
+  int32_t it;      // iteration counter j
+  uint32_t ticket; // last-CTA detection
+  int32_t pad2[2];
+};
+
+constexpr int VEC_BLOCK = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// CTA sum; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double s_w[VEC_BLOCK / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_w[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < VEC_BLOCK / 32 ? s_w[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// Writes the CTA partial; returns true in thread 0 of the last CTA, with the ordered total.
+__device__ __forceinline__ bool finish_reduction(double v, double* partials, uint32_t* ticket, double* total) {
+  __shared__ bool s_last;
+  double b = block_sum(v);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    uint32_t tk = atomicAdd(ticket, 1u);
+    s_last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  // last CTA: ordered sum of all partials
+  __threadfence();
+  double acc = 0.0;
+  for (int b2 = threadIdx.x; b2 < (int)gridDim.x; b2 += VEC_BLOCK) acc += ((volatile double*)partials)[b2];
+  // deterministic: fixed strided assignment + fixed tree
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) {
+    *total = acc;
+    *ticket = 0u;
+  }
+  return threadIdx.x == 0;
+}
+
+// r = b; p = b; x = 0; Ap = lam_init * p;  then partial r.r -> rr_new
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_init(const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r,
+        double* __restrict__ p, double* __restrict__ Ap, int64_t n, double lam_init,
+        double* partials, CgScalars* s) {
+  double acc = 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double v = b[l];
+    r[l] = v; p[l] = v; x[l] = 0.0; Ap[l] = lam_init * v;
+    acc = fma(v, v, acc);
+  }
+  double tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) {
+    s->rr_new = tot;
+    s->it = 0;
+  }
+}
+
+// p.Ap; the last CTA also rotates rr <- rr_new and records the history
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_dot_pAp(const double* __restrict__ p, const double* __restrict__ Ap, int64_t n,
+           double* partials, CgScalars* s, double* hist) {
+  double acc = 0.0;
+  const int64_t n2 = n >> 1;
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* a2 = reinterpret_cast<const double2*>(Ap);
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double2 pv = p2[l], av = a2[l];
+    acc = fma(pv.x, av.x, acc);
+    acc = fma(pv.y, av.y, acc);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) acc = fma(p[n - 1], Ap[n - 1], acc);
+  double tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) {
+    s->pAp = tot;
+    s->rr = s->rr_new;
+    if (hist) hist[s->it] = s->rr_new;
+  }
+}
+
+// alpha = rr / pAp;  x += alpha p;  r -= alpha Ap;  partial r.r -> rr_new
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_update_xr(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
+             const double* __restrict__ Ap, int64_t n, double* partials, CgScalars* s) {
+  const double pAp = s->pAp;
+  const double alpha = (pAp != 0.0) ? s->rr / pAp : 0.0;  // c15 guard
+  double acc = 0.0;
+  const int64_t n2 = n >> 1;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* a2 = reinterpret_cast<const double2*>(Ap);
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double2 xv = x2[l], pv = p2[l], rv = r2[l], av = a2[l];
+    xv.x = fma(alpha, pv.x, xv.x); xv.y = fma(alpha, pv.y, xv.y);
+    rv.x = fma(-alpha, av.x, rv.x); rv.y = fma(-alpha, av.y, rv.y);
+    x2[l] = xv; r2[l] = rv;
+    acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    x[l] = fma(alpha, p[l], x[l]);
+    double rv = fma(-alpha, Ap[l], r[l]);
+    r[l] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  double tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_new = tot;
+}
+
+// beta = rr_new / rr;  p = r + beta p;  Ap = lam_init p (assembly init of the next apply)
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_update_p(double* __restrict__ p, const double* __restrict__ r, double* __restrict__ Ap,
+            int64_t n, double lam_init, CgScalars* s) {
+  const double rr = s->rr;
+  const double beta = (rr != 0.0) ? s->rr_new / rr : 0.0;  // c15 guard
+  const int64_t n2 = n >> 1;
+  double2* p2 = reinterpret_cast<double2*>(p);
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double2* a2 = reinterpret_cast<double2*>(Ap);
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double2 pv = p2[l], rv = r2[l];
+    pv.x = fma(beta, pv.x, rv.x); pv.y = fma(beta, pv.y, rv.y);
+    p2[l] = pv;
+    a2[l] = make_double2(lam_init * pv.x, lam_init * pv.y);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    double pv = fma(beta, p[l], r[l]);
+    p[l] = pv; Ap[l] = lam_init * pv;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) s->it += 1;
+}
+
+// generic dot a.b -> *out (used by hb_dot)
+__global__ void __launch_bounds__(VEC_BLOCK)
+vec_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partials,
+        uint32_t* ticket, double* out) {
+  double acc = 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK)
+    acc = fma(a[l], b[l], acc);
+  double tot;
+  if (finish_reduction(acc, partials, ticket, &tot)) *out = tot;
+}
+
+// y = s * x
+__global__ void __launch_bounds__(VEC_BLOCK)
+vec_scale(const double* __restrict__ x, double* __restrict__ y, int64_t n, double s) {
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK)
+    y[l] = s * x[l];
+}
+
+// forcing b[l] = 2 (splitmix64(gid ^ seed) >> 11) 2^-53 - 1 (reading c12)
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(VEC_BLOCK)
+forcing_kernel(double* __restrict__ b, const int64_t* __restrict__ gids, int64_t n, uint64_t seed) {
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    uint64_t g = gids ? (uint64_t)gids[l] : (uint64_t)l;
+    uint64_t h = d_splitmix64(g ^ seed);
+    b[l] = 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
+  }
+}
+
+// 8:1 streaming kernel: each thread reads 8 fp64 and writes 1
+__global__ void __launch_bounds__(VEC_BLOCK)
+stream8to1(const double* __restrict__ in, double* __restrict__ out, int64_t n) {
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += __ldcs(in + (int64_t)k * n + l);
+    __stcs(out + l, s);
+  }
+}
+
+// halo pack: buf[t] = x[loc[t]]
+__global__ void __launch_bounds__(VEC_BLOCK)
+pack_kernel(const double* __restrict__ x, const int32_t* __restrict__ loc, double* __restrict__ buf, int64_t n) {
+  for (int64_t t = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; t < n; t += (int64_t)gridDim.x * VEC_BLOCK)
+    buf[t] = x[loc[t]];
+}
+
+// assembly unpack: y[loc[t]] += buf[t]  (entries of loc are distinct within one call)
+__global__ void __launch_bounds__(VEC_BLOCK)
+unpack_add_kernel(double* __restrict__ y, const int32_t* __restrict__ loc, const double* __restrict__ buf, int64_t n) {
+  for (int64_t t = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; t < n; t += (int64_t)gridDim.x * VEC_BLOCK)
+    atomicAdd(y + loc[t], buf[t]);
+}
+
+}  // namespace hbk
