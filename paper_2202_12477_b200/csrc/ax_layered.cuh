@@ -59,8 +59,16 @@ __device__ __forceinline__ void red_y(const AxArgs& a, int32_t g, double v) {
   else atomicAdd(a.y + g, v);
 }
 
-template <int N, bool HALO, bool MASSB>
-__global__ void __launch_bounds__(AxShape<N>::BLOCK)
+// L2 prefetch of a contiguous byte range by the bulk-copy engine (sm_90+): no registers,
+// no shared memory; keeps HBM streaming while the SM works on earlier elements.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// MINB: minimum resident CTAs per SM requested from ptxas (register cap); PF: L2 prefetch
+// distance in grid-stride waves (0 = off).
+template <int N, bool HALO, bool MASSB, int MINB = 1, int PF = 0>
+__global__ void __launch_bounds__(AxShape<N>::BLOCK, MINB)
 ax_layered(const AxArgs a) {
   using S = AxShape<N>;
   constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB;
@@ -96,7 +104,28 @@ ax_layered(const AxArgs a) {
 #define HB_DTJ(m) (S::DREG ? DTj[(m) < NP ? (m) : 0] : s_D[(m) * LDD + j])
   const bool interior_ij = (i > 0 && i < N && j > 0 && j < N);
 
+  if constexpr (PF > 0) {  // prime: the first PF waves
+    if (t == 0)
+      for (int w = 0; w < PF; ++w) {
+        const int64_t nb = a.e_begin + ((int64_t)blockIdx.x + (int64_t)w * gridDim.x) * EPB;
+        if (nb < a.e_end) {
+          const int64_t ne = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
+          prefetch_l2_bulk(a.G + nb * 6 * NP3, (uint32_t)(ne * 6 * NP3 * sizeof(double)));
+          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)((ne * NP3 * sizeof(int32_t) + 15) & ~15u));
+        }
+      }
+  }
   for (int64_t base = a.e_begin + (int64_t)blockIdx.x * EPB; base < a.e_end; base += (int64_t)gridDim.x * EPB) {
+    if constexpr (PF > 0) {
+      if (t == 0) {
+        const int64_t nb = base + (int64_t)PF * gridDim.x * EPB;
+        if (nb < a.e_end) {
+          const int64_t ne = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
+          prefetch_l2_bulk(a.G + nb * 6 * NP3, (uint32_t)(ne * 6 * NP3 * sizeof(double)));
+          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)((ne * NP3 * sizeof(int32_t) + 15) & ~15u));
+        }
+      }
+    }
     const int64_t e = base + le;
     const bool act = (e < a.e_end);
     int32_t gi[NP];

@@ -1,0 +1,278 @@
+// Fused screened-Poisson operator kernel, "line-owner" variant (sm_100a, all N).
+//
+//   Ap[g] (+)= sum_{(e,n): idx[e][n] = g} ( S_L^e u_e + lambda M_e u_e )[n],  u_e[n] = x[idx[e][n]]
+//
+// P:94-99   S_L^e = bold-D^T G^e bold-D, bold-D = [D(x)I(x)I; I(x)D(x)I; I(x)I(x)D]
+// P:100-108 six geometric factors per node (15 flops/node)
+// P:154     one kernel for (S_L + lambda W) Z x_G, here with Z^T fused (scatter-add)
+//
+// Every 1-D contraction is done by a thread that owns a whole line of N+1 values in
+// registers, so all lanes of a warp use the same entry of D at the same time: D is read from
+// shared memory with warp-uniform (broadcast) loads.  The GLL derivative matrix is
+// centro-antisymmetric, D[N-i][N-m] = -D[i][m] (so is D^T), which the contraction exploits
+// (even/odd folding): with e_m = u_m + u_{N-m}, o_m = u_m - u_{N-m},
+//   y_i = sum_m Mo[i][m] o_m + sum_m Me[i][m] e_m,  y_{N-i} = sum_m Mo o - sum_m Me e,
+//   Me[i][m] = (D[i][m] + D[i][N-m]) / 2,  Mo[i][m] = (D[i][m] - D[i][N-m]) / 2,
+// which halves the multiply-adds of the 12(N+1)^4 term (the FOM still counts P:110's flops).
+// Shared memory transposes between the three line orientations:
+//   P1  column owner (i,j): gather u[k] = x[idx] -> s_u; ut = D u (registers)
+//   P2  row owner (j,k): ur = D u_row -> s_r  and  (i,k) owner: us = D u_col -> s_s
+//   P3  column owner (i,j): (gr,gs,gt) = G (ur,us,ut) -> s_r, s_s in place, gt in registers
+//   P4  row owner: vr = D^T gr in place;  (i,k) owner: vs = D^T gs in place
+//   P5  column owner: out[k] = (D^T gt)[k] + vr + vs (+ lambda terms) -> store / RED
+// Padded layout s[k][j][i] with row pitch P1 and layer pitch P2 (offline bank-conflict
+// search) keeps all three orientations (nearly) conflict free.  G and idx of the element
+// group PF grid-waves ahead are prefetched into L2 by the bulk-copy engine, so HBM keeps
+// streaming while the SM computes.  Element-interior nodes (0<i,j,k<N) have one contributing
+// slot and W = 1: plain store; all other nodes use fp64 RED into an output pre-initialised
+// to lambda*x (reading R2).
+#pragma once
+#include <cstdint>
+
+#include "ax_layered.cuh"  // AxArgs, c_D, prefetch_l2_bulk, load_x / red_y
+
+namespace hbk {
+
+template <int N>
+struct LinesShape {
+  static constexpr int NP = N + 1;
+  static constexpr int NP2 = NP * NP;
+  static constexpr int NP3 = NP2 * NP;
+  static constexpr int EPB = (128 / NP2) > 0 ? (128 / NP2) : 1;
+  static constexpr int BLOCK = EPB * NP2;
+  // Shared-memory pitches (doubles) chosen by an offline bank-conflict search over the three
+  // access orientations (column, r-line, s-line) for this thread mapping; see DESIGN.md.
+  static constexpr int PAD[16][3] = {{0, 0, 0},       {2, 5, 12},      {3, 9, 27},       {4, 19, 76},
+                                     {5, 25, 125},    {9, 54, 324},    {7, 52, 369},     {9, 72, 576},
+                                     {9, 81, 729},    {10, 101, 1010}, {11, 121, 1331},  {13, 156, 1872},
+                                     {13, 169, 2197}, {17, 238, 3332}, {15, 225, 3375},  {17, 272, 4352}};
+  static constexpr int P1 = PAD[N][0];
+  static constexpr int P2 = PAD[N][1];
+  static constexpr int SLAB = PAD[N][2];  // doubles per element per buffer
+  // even/odd folded operator: H = (N+1)/2 row pairs, HE = H (+1 middle column if N+1 odd)
+  static constexpr int H = NP / 2, ODD = NP & 1, HE = H + ODD;
+  static constexpr int MAT = H * HE + H * H + H;  // Me, Mo, middle row
+  static constexpr int CONST = 2 * MAT;           // D and D^T
+  static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + ((CONST + 1) & ~1));
+  // resident CTAs per SM requested from ptxas: ~96 (N <= 7) / 128 registers per thread
+  // (enough for the line arrays), capped by the shared-memory footprint
+  static constexpr int REGS = N <= 7 ? 96 : 128;
+  static constexpr int MINB_REG = 65536 / (BLOCK * REGS) < 1 ? 1 : (65536 / (BLOCK * REGS) > 8 ? 8 : 65536 / (BLOCK * REGS));
+  static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
+  static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
+};
+
+// Build the folded matrices of M (M = D if !TRANS, M = D^T if TRANS) into s.
+template <int N, bool TRANS>
+__device__ __forceinline__ void eo_build(double* s, int t, int nthreads) {
+  using S = LinesShape<N>;
+  constexpr int NP = S::NP, H = S::H, HE = S::HE;
+  auto M = [](int i, int m) { return TRANS ? c_D[N][m * NP + i] : c_D[N][i * NP + m]; };
+  for (int q = t; q < S::MAT; q += nthreads) {
+    double v;
+    if (q < H * HE) {
+      const int i = q / HE, m = q % HE;
+      v = (m < H) ? 0.5 * (M(i, m) + M(i, N - m)) : M(i, m);  // m == H: middle column (odd NP)
+    } else if (q < H * HE + H * H) {
+      const int r = q - H * HE, i = r / H, m = r % H;
+      v = 0.5 * (M(i, m) - M(i, N - m));
+    } else {
+      const int m = q - H * HE - H * H;
+      v = M(H, m);  // middle row (odd NP): y_mid = sum_m M[mid][m] o_m
+    }
+    s[q] = v;
+  }
+}
+
+// y[l] = M x[l] for L lines at once (each uniform load of M feeds L multiply-adds).
+template <int N, int L>
+__device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const double (&x)[L][N + 1],
+                                         double (&y)[L][N + 1]) {
+  using S = LinesShape<N>;
+  constexpr int H = S::H, HE = S::HE, ODD = S::ODD;
+  const double* Me = sM;
+  const double* Mo = sM + H * HE;
+  const double* Mm = Mo + H * H;
+  double e[L][HE], o[L][H > 0 ? H : 1];
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      e[l][m] = x[l][m] + x[l][N - m];
+      o[l][m] = x[l][m] - x[l][N - m];
+    }
+    if constexpr (ODD) e[l][H] = x[l][H];
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double se[L], so[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) { se[l] = 0.0; so[l] = 0.0; }
+#pragma unroll
+    for (int m = 0; m < HE; ++m) {
+      const double cm = Me[i * HE + m];
+#pragma unroll
+      for (int l = 0; l < L; ++l) se[l] = fma(cm, e[l][m], se[l]);
+    }
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      const double cm = Mo[i * H + m];
+#pragma unroll
+      for (int l = 0; l < L; ++l) so[l] = fma(cm, o[l][m], so[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      y[l][i] = so[l] + se[l];
+      y[l][N - i] = so[l] - se[l];
+    }
+  }
+  if constexpr (ODD) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) y[l][H] = 0.0;
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      const double cm = Mm[m];
+#pragma unroll
+      for (int l = 0; l < L; ++l) y[l][H] = fma(cm, o[l][m], y[l][H]);
+    }
+  }
+}
+
+template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB>
+__global__ void __launch_bounds__(LinesShape<N>::BLOCK, MINB)
+ax_lines(const AxArgs a) {
+  using S = LinesShape<N>;
+  constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB, P1 = S::P1, P2 = S::P2, SLAB = S::SLAB;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x;
+  const int le = t / NP2;
+  const int c = t - le * NP2;
+  const int ca = c % NP, cb = c / NP;  // (i,j) for columns, (j,k) for rows, (i,k) for s-lines
+  double* s_u = smem + (0 * EPB + le) * SLAB;
+  double* s_r = smem + (1 * EPB + le) * SLAB;
+  double* s_s = smem + (2 * EPB + le) * SLAB;
+  double* s_D = smem + 3 * EPB * SLAB;  // folded D
+  double* s_DT = s_D + S::MAT;          // folded D^T
+  eo_build<N, false>(s_D, t, blockDim.x);
+  eo_build<N, true>(s_DT, t, blockDim.x);
+  const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
+
+  if constexpr (PF > 0) {
+    if (t == 0)
+      for (int w = 0; w < PF; ++w) {
+        const int64_t nb = a.e_begin + ((int64_t)blockIdx.x + (int64_t)w * gridDim.x) * EPB;
+        if (nb < a.e_end) {
+          const int64_t ne = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
+          prefetch_l2_bulk(a.G + nb * 6 * NP3, (uint32_t)(ne * 6 * NP3 * sizeof(double)));
+          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)((ne * NP3 * sizeof(int32_t) + 15) & ~15u));
+        }
+      }
+  }
+  __syncthreads();
+
+  for (int64_t base = a.e_begin + (int64_t)blockIdx.x * EPB; base < a.e_end; base += (int64_t)gridDim.x * EPB) {
+    if constexpr (PF > 0) {
+      if (t == 0) {
+        const int64_t nb = base + (int64_t)PF * gridDim.x * EPB;
+        if (nb < a.e_end) {
+          const int64_t ne = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
+          prefetch_l2_bulk(a.G + nb * 6 * NP3, (uint32_t)(ne * 6 * NP3 * sizeof(double)));
+          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)((ne * NP3 * sizeof(int32_t) + 15) & ~15u));
+        }
+      }
+    }
+    const int64_t e = base + le;
+    const bool act = (e < a.e_end);
+
+    // ---- P1: gather the (i,j) column (Z x) and the t-derivative in registers
+    int32_t gi[NP];
+    double gt[1][NP];  // ut, later the G-mixed gt
+    {
+      double col[1][NP];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) gi[k] = act ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
+        s_u[k * P2 + cb * P1 + ca] = col[0][k];
+      }
+      eo_apply<N, 1>(s_D, col, gt);
+    }
+    __syncthreads();
+
+    // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
+    {
+      double in[2][NP], out[2][NP];
+#pragma unroll
+      for (int m = 0; m < NP; ++m) {
+        in[0][m] = s_u[cb * P2 + ca * P1 + m];
+        in[1][m] = s_u[cb * P2 + m * P1 + ca];
+      }
+      eo_apply<N, 2>(s_D, in, out);
+#pragma unroll
+      for (int m = 0; m < NP; ++m) {
+        s_r[cb * P2 + ca * P1 + m] = out[0][m];
+        s_s[cb * P2 + m * P1 + ca] = out[1][m];
+      }
+    }
+    __syncthreads();
+
+    // ---- P3: metric at the (i,j) column nodes
+    {
+      const double* Ge = a.G + e * (6 * NP3) + c;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        double grr = 0, grs = 0, grt = 0, gss = 0, gst = 0, gtt = 0;
+        if (act) {
+          const double* g = Ge + k * 6 * NP2;
+          grr = __ldg(g); grs = __ldg(g + NP2); grt = __ldg(g + 2 * NP2);
+          gss = __ldg(g + 3 * NP2); gst = __ldg(g + 4 * NP2); gtt = __ldg(g + 5 * NP2);
+        }
+        const int o = k * P2 + cb * P1 + ca;
+        const double ur = s_r[o], us = s_s[o], ut = gt[0][k];
+        s_r[o] = grr * ur + grs * us + grt * ut;
+        s_s[o] = grs * ur + gss * us + gst * ut;
+        gt[0][k] = grt * ur + gst * us + gtt * ut;
+      }
+    }
+    __syncthreads();
+
+    // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
+    {
+      double in[2][NP], out[2][NP];
+#pragma unroll
+      for (int m = 0; m < NP; ++m) {
+        in[0][m] = s_r[cb * P2 + ca * P1 + m];
+        in[1][m] = s_s[cb * P2 + m * P1 + ca];
+      }
+      eo_apply<N, 2>(s_DT, in, out);
+#pragma unroll
+      for (int m = 0; m < NP; ++m) {
+        s_r[cb * P2 + ca * P1 + m] = out[0][m];
+        s_s[cb * P2 + m * P1 + ca] = out[1][m];
+      }
+    }
+    __syncthreads();
+
+    // ---- P5: t-direction transposed contraction, sum, assembly Z^T
+    if (act) {
+      double vt[1][NP];
+      eo_apply<N, 1>(s_DT, gt, vt);
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int o = k * P2 + cb * P1 + ca;
+        double out = vt[0][k] + s_r[o] + s_s[o];
+        if (MASSB) out = fma(a.lam * __ldg(a.B + e * NP3 + k * NP2 + c), s_u[o], out);
+        if (interior_ij && k > 0 && k < N) {
+          if (!MASSB) out = fma(a.lam, s_u[o], out);  // W = 1 on element-interior nodes
+          a.y[gi[k]] = out;                          // sole contribution: plain store
+        } else {
+          red_y<HALO>(a, gi[k], out);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace hbk

@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -24,6 +25,7 @@
 #include <vector>
 
 #include "ax_layered.cuh"
+#include "ax_lines.cuh"
 #include "internal.h"
 #include "vec.cuh"
 
@@ -33,6 +35,7 @@ using hb::set_error;
   do {                                                                                    \
     cudaError_t _e = (expr);                                                              \
     if (_e != cudaSuccess) {                                                              \
+      (void)cudaGetLastError(); /* clear the sticky last-error slot */                    \
       set_error(std::string(__func__) + ": " #expr ": " + cudaGetErrorString(_e));        \
       return (_e == cudaErrorMemoryAllocation) ? HB_ERR_OOM : HB_ERR_CUDA;                \
     }                                                                                     \
@@ -81,23 +84,52 @@ struct AxKernel {
   size_t smem = 0;
 };
 
-template <int N, bool HALO, bool MASSB>
+template <int N, bool HALO, bool MASSB, int MINB = 1, int PF = 0>
 AxKernel make_ax() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_layered<N, HALO, MASSB>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_layered<N, HALO, MASSB, MINB, PF>);
   k.block = hbk::AxShape<N>::BLOCK;
   k.epb = hbk::AxShape<N>::EPB;
   k.smem = hbk::AxShape<N>::SMEM;
   return k;
 }
 
+template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB>
+AxKernel make_lines() {
+  AxKernel k;
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB>);
+  k.block = hbk::LinesShape<N>::BLOCK;
+  k.epb = hbk::LinesShape<N>::EPB;
+  k.smem = hbk::LinesShape<N>::SMEM;
+  return k;
+}
+
+constexpr int kLinesPF = 1;  // L2 prefetch distance (grid waves)
+
 template <int N>
 AxKernel pick_ax_n(bool halo, bool massb) {
-  if (halo) return massb ? make_ax<N, true, true>() : make_ax<N, true, false>();
-  return massb ? make_ax<N, false, true>() : make_ax<N, false, false>();
+  if (halo) return massb ? make_lines<N, true, true, kLinesPF>() : make_lines<N, true, false, kLinesPF>();
+  return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
+}
+
+// experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
+AxKernel pick_ax_variant(int v) {
+  switch (v) {
+    case 1: return make_ax<7, false, false, 1, 0>();      // previous layered kernel
+    case 2: return make_lines<7, false, false, 0>();      // lines, no prefetch
+    case 3: return make_lines<7, false, false, 2>();      // lines, PF 2
+    case 4: return make_lines<7, false, false, 1, 4>();   // lines, PF 1, 4 CTAs/SM (128 regs)
+    case 5: return make_lines<7, false, false, 1, 6>();   // lines, PF 1, 6 CTAs/SM (85 regs)
+    case 6: return make_lines<7, false, false, 3>();      // lines, PF 3
+    default: return make_lines<7, false, false, kLinesPF>();
+  }
 }
 
 AxKernel pick_ax(int N, bool halo, bool massb) {
+  if (N == 7 && !halo && !massb) {
+    const char* v = getenv("HB_AX_VARIANT");
+    if (v && atoi(v) > 0) return pick_ax_variant(atoi(v));
+  }
   switch (N) {
     case 1: return pick_ax_n<1>(halo, massb);
     case 2: return pick_ax_n<2>(halo, massb);
@@ -181,6 +213,8 @@ struct hb_op {
   int64_t n_send = 0;
   AxKernel ax_plain, ax_halo;
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private stream for graph capture (the legacy stream cannot be captured)
+  cudaEvent_t ev_cap = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_haloel = nullptr, ev_gather = nullptr;
   cudaEvent_t ev_red = nullptr, ev_red_done = nullptr;
   // profiling
@@ -202,6 +236,8 @@ struct hb_op {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto& pr : prof_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (ev_cap) cudaEventDestroy(ev_cap);
     for (cudaEvent_t e : {ev_pack, ev_halo, ev_haloel, ev_gather, ev_red, ev_red_done}) if (e) cudaEventDestroy(e);
     if (host_scal) cudaFreeHost(host_scal);
   }
@@ -445,7 +481,8 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU_TRY(cudaStreamCreateWithPriority(&op->comm_stream, cudaStreamNonBlocking, hi));
   }
-  for (cudaEvent_t* e : {&op->ev_pack, &op->ev_halo, &op->ev_haloel, &op->ev_gather, &op->ev_red, &op->ev_red_done})
+  CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&op->ev_pack, &op->ev_halo, &op->ev_haloel, &op->ev_gather, &op->ev_red, &op->ev_red_done, &op->ev_cap})
     CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CU_TRY(cudaStreamSynchronize(st));
   return HB_OK;
@@ -593,10 +630,11 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
   if (it == op->graphs.end()) {
     int64_t l0 = op->launches;
     cudaGraph_t graph;
-    CU_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int status = cg_init(op, b, x, st);
-    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, st);
-    cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    cudaStream_t cs = op->cap_stream;
+    CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int status = cg_init(op, b, x, cs);
+    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
+    cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
     CU_TRY(ce);
     cudaGraphExec_t exec;
