@@ -29,70 +29,100 @@
 #pragma once
 #include <cstdint>
 
-#include "ax_layered.cuh"  // AxArgs, c_D, prefetch_l2_bulk, load_x / red_y
+#include "common.cuh"  // AxArgs, c_D, prefetch_l2_bulk, load_x / red_y
 
 namespace hbk {
 
-template <int N>
+template <int N, int EPBX = 0>
 struct LinesShape {
   static constexpr int NP = N + 1;
   static constexpr int NP2 = NP * NP;
   static constexpr int NP3 = NP2 * NP;
-  static constexpr int EPB = (128 / NP2) > 0 ? (128 / NP2) : 1;
+  // ~64 threads per CTA (one element from N = 7 up): fine-grained CTAs balance best
+  static constexpr int EPB = EPBX > 0 ? EPBX : ((64 / NP2) > 0 ? (64 / NP2) : 1);
   static constexpr int BLOCK = EPB * NP2;
-  // Shared-memory pitches (doubles) chosen by an offline bank-conflict search over the three
-  // access orientations (column, r-line, s-line) for this thread mapping; see DESIGN.md.
+  // Shared-memory layout of one element buffer: (i,j,k) -> doubles.  NP = 8 and NP = 16 use an
+  // XOR swizzle that makes all three line orientations conflict free; other N use row / layer
+  // padding from an offline bank-conflict search.
   static constexpr int PAD[16][3] = {{0, 0, 0},       {2, 5, 12},      {3, 9, 27},       {4, 19, 76},
-                                     {5, 25, 125},    {9, 54, 324},    {7, 52, 369},     {9, 72, 576},
+                                     {5, 25, 125},    {9, 54, 324},    {7, 52, 369},     {8, 72, 576},
                                      {9, 81, 729},    {10, 101, 1010}, {11, 121, 1331},  {13, 156, 1872},
-                                     {13, 169, 2197}, {17, 238, 3332}, {15, 225, 3375},  {17, 272, 4352}};
+                                     {13, 169, 2197}, {17, 238, 3332}, {15, 225, 3375},  {16, 256, 4096}};
   static constexpr int P1 = PAD[N][0];
   static constexpr int P2 = PAD[N][1];
-  static constexpr int SLAB = PAD[N][2];  // doubles per element per buffer
-  // even/odd folded operator: H = (N+1)/2 row pairs, HE = H (+1 middle column if N+1 odd)
+  static constexpr int SLAB = PAD[N][2] + (PAD[N][2] & 1);  // doubles per element per buffer (even)
+  __device__ __forceinline__ static int at(int i, int j, int k) {
+    if constexpr (N == 7) return k * 72 + j * 8 + (i ^ (((j >> 1) + 4 * (k & 1)) & 7));
+    else if constexpr (N == 15) return k * 256 + j * 16 + (i ^ j);
+    else return k * P2 + j * P1 + i;
+  }
+  // even/odd folded operator: H = (N+1)/2 row pairs, HE = H (+1 middle column if N+1 odd);
+  // rows padded to even length so pairs load as one 16-byte broadcast
   static constexpr int H = NP / 2, ODD = NP & 1, HE = H + ODD;
-  static constexpr int MAT = H * HE + H * H + H;  // Me, Mo, middle row
-  static constexpr int CONST = 2 * MAT;           // D and D^T
-  static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + ((CONST + 1) & ~1));
+  static constexpr int HE2 = HE + (HE & 1), H2 = H + (H & 1);
+  static constexpr int MAT = H * HE2 + H * H2 + H2;  // Me, Mo, middle row
+  static constexpr int CONST = 2 * MAT;               // D and D^T
+  static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
   // resident CTAs per SM requested from ptxas: ~96 (N <= 7) / 128 registers per thread
-  // (enough for the line arrays), capped by the shared-memory footprint
+  // (enough for the line arrays), capped by the shared-memory footprint and 32 CTAs/SM
   static constexpr int REGS = N <= 7 ? 96 : 128;
-  static constexpr int MINB_REG = 65536 / (BLOCK * REGS) < 1 ? 1 : (65536 / (BLOCK * REGS) > 8 ? 8 : 65536 / (BLOCK * REGS));
+  static constexpr int MINB_REG0 = 65536 / (BLOCK * REGS);
+  static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
 };
 
-// Build the folded matrices of M (M = D if !TRANS, M = D^T if TRANS) into s.
-template <int N, bool TRANS>
+// Build the folded matrices of M (M = D if !TRANS, M = D^T if TRANS) into s (zero padded).
+template <int N, int EPBX, bool TRANS>
 __device__ __forceinline__ void eo_build(double* s, int t, int nthreads) {
-  using S = LinesShape<N>;
-  constexpr int NP = S::NP, H = S::H, HE = S::HE;
+  using S = LinesShape<N, EPBX>;
+  constexpr int NP = S::NP, H = S::H, HE = S::HE, HE2 = S::HE2, H2 = S::H2;
   auto M = [](int i, int m) { return TRANS ? c_D[N][m * NP + i] : c_D[N][i * NP + m]; };
   for (int q = t; q < S::MAT; q += nthreads) {
-    double v;
-    if (q < H * HE) {
-      const int i = q / HE, m = q % HE;
-      v = (m < H) ? 0.5 * (M(i, m) + M(i, N - m)) : M(i, m);  // m == H: middle column (odd NP)
-    } else if (q < H * HE + H * H) {
-      const int r = q - H * HE, i = r / H, m = r % H;
-      v = 0.5 * (M(i, m) - M(i, N - m));
+    double v = 0.0;
+    if (q < H * HE2) {
+      const int i = q / HE2, m = q % HE2;
+      if (m < H) v = 0.5 * (M(i, m) + M(i, N - m));
+      else if (m < HE) v = M(i, m);  // m == H: middle column (odd NP)
+    } else if (q < H * HE2 + H * H2) {
+      const int r = q - H * HE2, i = r / H2, m = r % H2;
+      if (m < H) v = 0.5 * (M(i, m) - M(i, N - m));
     } else {
-      const int m = q - H * HE - H * H;
-      v = M(H, m);  // middle row (odd NP): y_mid = sum_m M[mid][m] o_m
+      const int m = q - H * HE2 - H * H2;
+      if (S::ODD && m < H) v = M(H, m);  // middle row (odd NP): y_mid = sum_m M[mid][m] o_m
     }
     s[q] = v;
   }
 }
 
+// sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs
+template <int CNT, int L, int W>
+__device__ __forceinline__ void dot_rows(const double* __restrict__ C, const double (&v)[L][W], double (&acc)[L]) {
+#pragma unroll
+  for (int m = 0; m + 1 < CNT; m += 2) {
+    const double2 c2 = *reinterpret_cast<const double2*>(C + m);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      acc[l] = fma(c2.x, v[l][m], acc[l]);
+      acc[l] = fma(c2.y, v[l][m + 1], acc[l]);
+    }
+  }
+  if constexpr (CNT & 1) {
+    const double cl = C[CNT - 1];
+#pragma unroll
+    for (int l = 0; l < L; ++l) acc[l] = fma(cl, v[l][CNT - 1], acc[l]);
+  }
+}
+
 // y[l] = M x[l] for L lines at once (each uniform load of M feeds L multiply-adds).
-template <int N, int L>
+template <int N, int EPBX, int L>
 __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const double (&x)[L][N + 1],
                                          double (&y)[L][N + 1]) {
-  using S = LinesShape<N>;
-  constexpr int H = S::H, HE = S::HE, ODD = S::ODD;
+  using S = LinesShape<N, EPBX>;
+  constexpr int H = S::H, HE = S::HE, ODD = S::ODD, HE2 = S::HE2, H2 = S::H2;
   const double* Me = sM;
-  const double* Mo = sM + H * HE;
-  const double* Mm = Mo + H * H;
+  const double* Mo = sM + H * HE2;
+  const double* Mm = Mo + H * H2;
   double e[L][HE], o[L][H > 0 ? H : 1];
 #pragma unroll
   for (int l = 0; l < L; ++l) {
@@ -108,18 +138,8 @@ __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const do
     double se[L], so[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) { se[l] = 0.0; so[l] = 0.0; }
-#pragma unroll
-    for (int m = 0; m < HE; ++m) {
-      const double cm = Me[i * HE + m];
-#pragma unroll
-      for (int l = 0; l < L; ++l) se[l] = fma(cm, e[l][m], se[l]);
-    }
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const double cm = Mo[i * H + m];
-#pragma unroll
-      for (int l = 0; l < L; ++l) so[l] = fma(cm, o[l][m], so[l]);
-    }
+    dot_rows<HE, L, HE>(Me + i * HE2, e, se);
+    dot_rows<H, L, (H > 0 ? H : 1)>(Mo + i * H2, o, so);
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       y[l][i] = so[l] + se[l];
@@ -127,22 +147,20 @@ __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const do
     }
   }
   if constexpr (ODD) {
+    double sm[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) y[l][H] = 0.0;
+    for (int l = 0; l < L; ++l) sm[l] = 0.0;
+    dot_rows<H, L, (H > 0 ? H : 1)>(Mm, o, sm);
 #pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const double cm = Mm[m];
-#pragma unroll
-      for (int l = 0; l < L; ++l) y[l][H] = fma(cm, o[l][m], y[l][H]);
-    }
+    for (int l = 0; l < L; ++l) y[l][H] = sm[l];
   }
 }
 
-template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB>
-__global__ void __launch_bounds__(LinesShape<N>::BLOCK, MINB)
+template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0>
+__global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
-  using S = LinesShape<N>;
-  constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB, P1 = S::P1, P2 = S::P2, SLAB = S::SLAB;
+  using S = LinesShape<N, EPBX>;
+  constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB, SLAB = S::SLAB;
   extern __shared__ double smem[];
   const int t = threadIdx.x;
   const int le = t / NP2;
@@ -153,8 +171,8 @@ ax_lines(const AxArgs a) {
   double* s_s = smem + (2 * EPB + le) * SLAB;
   double* s_D = smem + 3 * EPB * SLAB;  // folded D
   double* s_DT = s_D + S::MAT;          // folded D^T
-  eo_build<N, false>(s_D, t, blockDim.x);
-  eo_build<N, true>(s_DT, t, blockDim.x);
+  eo_build<N, EPBX, false>(s_D, t, blockDim.x);
+  eo_build<N, EPBX, true>(s_DT, t, blockDim.x);
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
 
   if constexpr (PF > 0) {
@@ -164,7 +182,7 @@ ax_lines(const AxArgs a) {
         if (nb < a.e_end) {
           const int64_t ne = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
           prefetch_l2_bulk(a.G + nb * 6 * NP3, (uint32_t)(ne * 6 * NP3 * sizeof(double)));
-          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)((ne * NP3 * sizeof(int32_t) + 15) & ~15u));
+          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)(ne * NP3 * sizeof(int32_t)));
         }
       }
   }
@@ -177,7 +195,7 @@ ax_lines(const AxArgs a) {
         if (nb < a.e_end) {
           const int64_t ne = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
           prefetch_l2_bulk(a.G + nb * 6 * NP3, (uint32_t)(ne * 6 * NP3 * sizeof(double)));
-          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)((ne * NP3 * sizeof(int32_t) + 15) & ~15u));
+          prefetch_l2_bulk(a.idx + nb * NP3, (uint32_t)(ne * NP3 * sizeof(int32_t)));
         }
       }
     }
@@ -194,9 +212,9 @@ ax_lines(const AxArgs a) {
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
-        s_u[k * P2 + cb * P1 + ca] = col[0][k];
+        s_u[S::at(ca, cb, k)] = col[0][k];
       }
-      eo_apply<N, 1>(s_D, col, gt);
+      eo_apply<N, EPBX, 1>(s_D, col, gt);
     }
     __syncthreads();
 
@@ -205,14 +223,14 @@ ax_lines(const AxArgs a) {
       double in[2][NP], out[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
-        in[0][m] = s_u[cb * P2 + ca * P1 + m];
-        in[1][m] = s_u[cb * P2 + m * P1 + ca];
+        in[0][m] = s_u[S::at(m, ca, cb)];
+        in[1][m] = s_u[S::at(ca, m, cb)];
       }
-      eo_apply<N, 2>(s_D, in, out);
+      eo_apply<N, EPBX, 2>(s_D, in, out);
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
-        s_r[cb * P2 + ca * P1 + m] = out[0][m];
-        s_s[cb * P2 + m * P1 + ca] = out[1][m];
+        s_r[S::at(m, ca, cb)] = out[0][m];
+        s_s[S::at(ca, m, cb)] = out[1][m];
       }
     }
     __syncthreads();
@@ -228,7 +246,7 @@ ax_lines(const AxArgs a) {
           grr = __ldg(g); grs = __ldg(g + NP2); grt = __ldg(g + 2 * NP2);
           gss = __ldg(g + 3 * NP2); gst = __ldg(g + 4 * NP2); gtt = __ldg(g + 5 * NP2);
         }
-        const int o = k * P2 + cb * P1 + ca;
+        const int o = S::at(ca, cb, k);
         const double ur = s_r[o], us = s_s[o], ut = gt[0][k];
         s_r[o] = grr * ur + grs * us + grt * ut;
         s_s[o] = grs * ur + gss * us + gst * ut;
@@ -242,14 +260,14 @@ ax_lines(const AxArgs a) {
       double in[2][NP], out[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
-        in[0][m] = s_r[cb * P2 + ca * P1 + m];
-        in[1][m] = s_s[cb * P2 + m * P1 + ca];
+        in[0][m] = s_r[S::at(m, ca, cb)];
+        in[1][m] = s_s[S::at(ca, m, cb)];
       }
-      eo_apply<N, 2>(s_DT, in, out);
+      eo_apply<N, EPBX, 2>(s_DT, in, out);
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
-        s_r[cb * P2 + ca * P1 + m] = out[0][m];
-        s_s[cb * P2 + m * P1 + ca] = out[1][m];
+        s_r[S::at(m, ca, cb)] = out[0][m];
+        s_s[S::at(ca, m, cb)] = out[1][m];
       }
     }
     __syncthreads();
@@ -257,10 +275,10 @@ ax_lines(const AxArgs a) {
     // ---- P5: t-direction transposed contraction, sum, assembly Z^T
     if (act) {
       double vt[1][NP];
-      eo_apply<N, 1>(s_DT, gt, vt);
+      eo_apply<N, EPBX, 1>(s_DT, gt, vt);
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        const int o = k * P2 + cb * P1 + ca;
+        const int o = S::at(ca, cb, k);
         double out = vt[0][k] + s_r[o] + s_s[o];
         if (MASSB) out = fma(a.lam * __ldg(a.B + e * NP3 + k * NP2 + c), s_u[o], out);
         if (interior_ij && k > 0 && k < N) {

@@ -24,7 +24,6 @@
 #include <tuple>
 #include <vector>
 
-#include "ax_layered.cuh"
 #include "ax_lines.cuh"
 #include "internal.h"
 #include "vec.cuh"
@@ -84,27 +83,17 @@ struct AxKernel {
   size_t smem = 0;
 };
 
-template <int N, bool HALO, bool MASSB, int MINB = 1, int PF = 0>
-AxKernel make_ax() {
-  AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_layered<N, HALO, MASSB, MINB, PF>);
-  k.block = hbk::AxShape<N>::BLOCK;
-  k.epb = hbk::AxShape<N>::EPB;
-  k.smem = hbk::AxShape<N>::SMEM;
-  return k;
-}
-
-template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB>
+template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB>);
-  k.block = hbk::LinesShape<N>::BLOCK;
-  k.epb = hbk::LinesShape<N>::EPB;
-  k.smem = hbk::LinesShape<N>::SMEM;
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX>);
+  k.block = hbk::LinesShape<N, EPBX>::BLOCK;
+  k.epb = hbk::LinesShape<N, EPBX>::EPB;
+  k.smem = hbk::LinesShape<N, EPBX>::SMEM;
   return k;
 }
 
-constexpr int kLinesPF = 1;  // L2 prefetch distance (grid waves)
+constexpr int kLinesPF = 0;  // L2 bulk prefetch distance (grid waves); measured slower on B200
 
 template <int N>
 AxKernel pick_ax_n(bool halo, bool massb) {
@@ -115,12 +104,10 @@ AxKernel pick_ax_n(bool halo, bool massb) {
 // experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
 AxKernel pick_ax_variant(int v) {
   switch (v) {
-    case 1: return make_ax<7, false, false, 1, 0>();      // previous layered kernel
-    case 2: return make_lines<7, false, false, 0>();      // lines, no prefetch
-    case 3: return make_lines<7, false, false, 2>();      // lines, PF 2
-    case 4: return make_lines<7, false, false, 1, 4>();   // lines, PF 1, 4 CTAs/SM (128 regs)
-    case 5: return make_lines<7, false, false, 1, 6>();   // lines, PF 1, 6 CTAs/SM (85 regs)
-    case 6: return make_lines<7, false, false, 3>();      // lines, PF 3
+    case 1: return make_lines<7, false, false, 0, 8, 1>();   // 128 regs
+    case 2: return make_lines<7, false, false, 0, 12, 1>();  // 85 regs
+    case 3: return make_lines<7, false, false, 0, 5, 2>();   // 2 elements / CTA
+    case 4: return make_lines<7, false, false, 1, 10, 1>();  // + L2 bulk prefetch
     default: return make_lines<7, false, false, kLinesPF>();
   }
 }
@@ -245,6 +232,15 @@ struct hb_op {
 
 namespace {
 
+// timing event: an external event node while the stream is being captured, else a plain record
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, st);
+}
+
 int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double* x, double* y, cudaStream_t st) {
   if (e1 <= e0) return HB_OK;
   hbk::AxArgs a;
@@ -272,11 +268,11 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
     e_start = op->prof_events[op->prof_used].first;
     e_stop = op->prof_events[op->prof_used].second;
     op->prof_used++;
-    CU_TRY(cudaEventRecordWithFlags(e_start, st, cudaEventRecordExternal));
+    CU_TRY(record_event(e_start, st));
   }
   CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
   op->launches++;
-  if (op->profiling) CU_TRY(cudaEventRecordWithFlags(e_stop, st, cudaEventRecordExternal));
+  if (op->profiling) CU_TRY(record_event(e_stop, st));
   return HB_OK;
 }
 
