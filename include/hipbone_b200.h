@@ -157,9 +157,10 @@ int hb_cg_solve(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters
  * x back; copies are inside the call (end-to-end path). */
 int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t max_iters, double eps,
                      double* rr_hist_host, hb_cg_result* res, void* stream);
-/* Profiling of the operator kernel inside hb_cg_solve / hb_op_apply: when enabled, CUDA
- * events bracket every operator launch on its stream; hb_op_kernel_time returns the
- * number of timed launches and their mean duration in seconds since the last reset. */
+/* Profiling of the operator kernel inside hb_cg_solve / hb_op_apply: enable = k > 0 brackets
+ * every k-th operator launch with CUDA events on its stream (inside captured graphs as event
+ * nodes); enable = 0 turns it off.  hb_op_kernel_time returns the number of timed launches
+ * of the last solve (or since enabling, outside graphs) and their mean duration in seconds. */
 int hb_op_set_profiling(hb_op* op, int enable);
 int hb_op_kernel_time(hb_op* op, int64_t* launches, double* mean_seconds);
 /* Launch statistics: number of library kernels launched since creation. */

@@ -61,7 +61,8 @@ struct LinesShape {
   static constexpr int H = NP / 2, ODD = NP & 1, HE = H + ODD;
   static constexpr int HE2 = HE + (HE & 1), H2 = H + (H & 1);
   static constexpr int MAT = H * HE2 + H * H2 + H2;  // Me, Mo, middle row
-  static constexpr int CONST = 2 * MAT;               // D and D^T
+  static constexpr int CONST = 2 * MAT;               // D and D^T (host-built, g_EO[N])
+  static_assert(CONST <= EO_MAX, "folded D table");
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
   // resident CTAs per SM requested from ptxas: ~96 (N <= 7) / 128 registers per thread
   // (enough for the line arrays), capped by the shared-memory footprint and 32 CTAs/SM
@@ -71,29 +72,6 @@ struct LinesShape {
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
 };
-
-// Build the folded matrices of M (M = D if !TRANS, M = D^T if TRANS) into s (zero padded).
-template <int N, int EPBX, bool TRANS>
-__device__ __forceinline__ void eo_build(double* s, int t, int nthreads) {
-  using S = LinesShape<N, EPBX>;
-  constexpr int NP = S::NP, H = S::H, HE = S::HE, HE2 = S::HE2, H2 = S::H2;
-  auto M = [](int i, int m) { return TRANS ? c_D[N][m * NP + i] : c_D[N][i * NP + m]; };
-  for (int q = t; q < S::MAT; q += nthreads) {
-    double v = 0.0;
-    if (q < H * HE2) {
-      const int i = q / HE2, m = q % HE2;
-      if (m < H) v = 0.5 * (M(i, m) + M(i, N - m));
-      else if (m < HE) v = M(i, m);  // m == H: middle column (odd NP)
-    } else if (q < H * HE2 + H * H2) {
-      const int r = q - H * HE2, i = r / H2, m = r % H2;
-      if (m < H) v = 0.5 * (M(i, m) - M(i, N - m));
-    } else {
-      const int m = q - H * HE2 - H * H2;
-      if (S::ODD && m < H) v = M(H, m);  // middle row (odd NP): y_mid = sum_m M[mid][m] o_m
-    }
-    s[q] = v;
-  }
-}
 
 // sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs
 template <int CNT, int L, int W>
@@ -156,7 +134,58 @@ __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const do
   }
 }
 
-template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0>
+// Fused p.Ap (P:217's dot, computed as the element energy): CTA tree sum in shared memory,
+// one partial per CTA, the last CTA sums the partials in CTA order (deterministic) and either
+// accumulates (more launches of this apply follow) or publishes p.Ap = e + lambda p.p and
+// rotates r.r (the bookkeeping a separate p.Ap kernel would do).
+template <int BLOCK>
+__device__ __forceinline__ void energy_finish(double en, const AxArgs& a, double* red) {
+  __shared__ bool s_last;
+  const int t = threadIdx.x;
+  red[t] = en;
+  __syncthreads();
+  constexpr int P2B = BLOCK <= 1 ? 1 : (BLOCK <= 2 ? 2 : (BLOCK <= 4 ? 4 : (BLOCK <= 8 ? 8 : (BLOCK <= 16 ? 16 :
+                      (BLOCK <= 32 ? 32 : (BLOCK <= 64 ? 64 : (BLOCK <= 128 ? 128 : 256)))))));
+#pragma unroll
+  for (int h = P2B / 2; h > 0; h >>= 1) {
+    if (t < h && t + h < BLOCK) red[t] += red[t + h];
+    __syncthreads();
+  }
+  if (t == 0) {
+    a.e_part[blockIdx.x] = red[0];
+    __threadfence();
+    s_last = (atomicAdd(&a.cg->ticket_e, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last CTA: ordered sum of the partials (fixed strided assignment + fixed tree)
+  double v = 0.0;
+  const volatile double* pv = a.e_part;
+  for (unsigned b = t; b < gridDim.x; b += BLOCK) v += pv[b];
+  red[t] = v;
+  __syncthreads();
+#pragma unroll
+  for (int h = P2B / 2; h > 0; h >>= 1) {
+    if (t < h && t + h < BLOCK) red[t] += red[t + h];
+    __syncthreads();
+  }
+  if (t == 0) {
+    const double tot = red[0];
+    CgScalars* s = a.cg;
+    s->ticket_e = 0u;
+    if (a.e_final) {
+      s->pAp = s->e_acc + tot + a.lam_pp * s->pp;
+      s->e_acc = 0.0;
+      s->rr = s->rr_new;
+      if (a.hist) a.hist[s->it] = s->rr_new;
+    } else {
+      s->e_acc += tot;
+    }
+  }
+}
+
+template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0, bool PFL = true>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
@@ -171,9 +200,9 @@ ax_lines(const AxArgs a) {
   double* s_s = smem + (2 * EPB + le) * SLAB;
   double* s_D = smem + 3 * EPB * SLAB;  // folded D
   double* s_DT = s_D + S::MAT;          // folded D^T
-  eo_build<N, EPBX, false>(s_D, t, blockDim.x);
-  eo_build<N, EPBX, true>(s_DT, t, blockDim.x);
+  for (int q = t; q < S::CONST; q += S::BLOCK) s_D[q] = __ldg(&g_EO[N][q]);  // folded D | D^T
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
+  double en = 0.0;  // element energy u.(S_e u) (+ lambda u.B u) of this thread's nodes
 
   if constexpr (PF > 0) {
     if (t == 0)
@@ -201,6 +230,20 @@ ax_lines(const AxArgs a) {
     }
     const int64_t e = base + le;
     const bool act = (e < a.e_end);
+
+    // Early L2 prefetch of this element's geometric factors (consumed in P3, after the
+    // gather and two barriers) and of the next element's index block (next P1).
+    if constexpr (PFL) {
+      if (act) {
+        const char* gb = reinterpret_cast<const char*>(a.G + e * (6 * NP3));
+        for (int q = t - le * NP2; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(gb + q * 128);
+        const int64_t en = e + (int64_t)gridDim.x * EPB;
+        if (en < a.e_end) {
+          const char* ib = reinterpret_cast<const char*>(a.idx + en * NP3);
+          for (int q = c; q < (NP3 * 4 + 127) / 128; q += NP2) prefetch_l2_line(ib + q * 128);
+        }
+      }
+    }
 
     // ---- P1: gather the (i,j) column (Z x) and the t-derivative in registers
     int32_t gi[NP];
@@ -280,9 +323,15 @@ ax_lines(const AxArgs a) {
       for (int k = 0; k < NP; ++k) {
         const int o = S::at(ca, cb, k);
         double out = vt[0][k] + s_r[o] + s_s[o];
-        if (MASSB) out = fma(a.lam * __ldg(a.B + e * NP3 + k * NP2 + c), s_u[o], out);
+        const double uk = s_u[o];
+        en = fma(uk, out, en);
+        if (MASSB) {
+          const double lb = a.lam * __ldg(a.B + e * NP3 + k * NP2 + c) * uk;
+          out += lb;
+          en = fma(uk, lb, en);
+        }
         if (interior_ij && k > 0 && k < N) {
-          if (!MASSB) out = fma(a.lam, s_u[o], out);  // W = 1 on element-interior nodes
+          if (!MASSB) out = fma(a.lam, uk, out);  // W = 1 on element-interior nodes
           a.y[gi[k]] = out;                          // sole contribution: plain store
         } else {
           red_y<HALO>(a, gi[k], out);
@@ -291,6 +340,7 @@ ax_lines(const AxArgs a) {
     }
     __syncthreads();
   }
+  if (a.cg) energy_finish<S::BLOCK>(en, a, smem);
 }
 
 }  // namespace hbk

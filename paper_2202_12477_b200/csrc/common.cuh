@@ -7,6 +7,23 @@ namespace hbk {
 
 
 __constant__ double c_D[16][256];  // c_D[N][i*(N+1)+j] = D_ij for N = 1..15
+// even/odd folded D and D^T per N (layout in ax_lines.cuh LinesShape), written by the host
+constexpr int EO_MAX = 272;
+__device__ double g_EO[16][EO_MAX];
+
+// Device-resident CG scalars (alpha, beta are never sent to the host; see vec.cuh)
+struct CgScalars {
+  double pAp;      // p.Ap (global after allreduce)
+  double rr;       // r_j.r_j
+  double rr_new;   // r_{j+1}.r_{j+1} (global after allreduce)
+  double pp;       // local p.p (for the lambda term of the fused p.Ap)
+  double e_acc;    // element-energy accumulator across the operator launches of one apply
+  double pad[3];
+  int32_t it;        // iteration counter j
+  uint32_t ticket;   // last-CTA detection, vector kernels
+  uint32_t ticket_e; // last-CTA detection, operator energy
+  int32_t pad2;
+};
 
 struct AxArgs {
   const int32_t* __restrict__ idx;  // [E][NP3] local index into [owned | halo]
@@ -19,6 +36,12 @@ struct AxArgs {
   int64_t e_begin, e_end;           // element range of this launch
   int32_t n_owned;
   double lam;
+  // fused p.Ap (CG only; cg == nullptr otherwise): p.Ap = sum_e u_e^T S_e u_e + lambda p.p
+  CgScalars* cg;
+  double* e_part;   // per-CTA partial energies
+  double* hist;     // r.r history (written with the rr rotation by the final launch)
+  double lam_pp;    // lambda (mass mode 0) or 0 (mode 1: lambda B is in the element energy)
+  int32_t e_final;  // this launch completes the apply: publish p.Ap
 };
 
 template <bool HALO>
@@ -40,6 +63,11 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
   const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
+
+// Per-thread L2 prefetch of one 128-byte line (no registers, no completion tracking).
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 }  // namespace hbk

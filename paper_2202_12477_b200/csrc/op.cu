@@ -83,10 +83,10 @@ struct AxKernel {
   size_t smem = 0;
 };
 
-template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0>
+template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0, bool PFL = true>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
@@ -104,10 +104,9 @@ AxKernel pick_ax_n(bool halo, bool massb) {
 // experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
 AxKernel pick_ax_variant(int v) {
   switch (v) {
-    case 1: return make_lines<7, false, false, 0, 8, 1>();   // 128 regs
-    case 2: return make_lines<7, false, false, 0, 12, 1>();  // 85 regs
-    case 3: return make_lines<7, false, false, 0, 5, 2>();   // 2 elements / CTA
-    case 4: return make_lines<7, false, false, 1, 10, 1>();  // + L2 bulk prefetch
+    case 1: return make_lines<7, false, false, 0, 10, 0, false>();  // no per-element L2 prefetch
+    case 2: return make_lines<7, false, false, 0, 8, 1>();          // 128 regs
+    case 3: return make_lines<7, false, false, 0, 12, 1>();         // 80 regs
     default: return make_lines<7, false, false, kLinesPF>();
   }
 }
@@ -193,7 +192,7 @@ struct hb_op {
   int64_t nA = 0, nH = 0, nB = 0;
   // device data
   DevBuf idx, G, B, owned_gid;
-  DevBuf r, p, Ap, xs, partials, scal, hist, dot_out, dot_ticket;
+  DevBuf r, p, Ap, xs, partials, e_part, scal, hist, dot_out, dot_ticket;
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
   std::vector<int32_t> nbr;
   std::vector<int64_t> soff, scnt, roff, rcnt;
@@ -206,6 +205,8 @@ struct hb_op {
   cudaEvent_t ev_red = nullptr, ev_red_done = nullptr;
   // profiling
   bool profiling = false;
+  int prof_stride = 1;      // time every prof_stride-th operator launch
+  int64_t prof_seq = 0;     // operator launches seen since profiling was (re)enabled
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   int64_t launches = 0;
@@ -241,7 +242,8 @@ cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
                                              : cudaEventRecord(ev, st);
 }
 
-int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double* x, double* y, cudaStream_t st) {
+int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double* x, double* y, cudaStream_t st,
+              bool energy = false, bool final_launch = false) {
   if (e1 <= e0) return HB_OK;
   hbk::AxArgs a;
   a.idx = op->idx.as<int32_t>();
@@ -254,11 +256,17 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.e_begin = e0; a.e_end = e1;
   a.n_owned = (int32_t)op->sz.n_owned;
   a.lam = op->lam;
+  a.cg = energy ? op->scal.as<hbk::CgScalars>() : nullptr;
+  a.e_part = op->e_part.as<double>();
+  a.hist = op->hist.as<double>();
+  a.lam_pp = op->mass_mode == 0 ? op->lam : 0.0;
+  a.e_final = final_launch ? 1 : 0;
   int64_t groups = (e1 - e0 + k.epb - 1) / k.epb;
   int grid = (int)std::min<int64_t>(groups, (int64_t)k.grid_max);
   void* args[] = {&a};
   cudaEvent_t e_start = nullptr, e_stop = nullptr;
-  if (op->profiling) {
+  const bool timed = op->profiling && (op->prof_seq++ % op->prof_stride == 0);
+  if (timed) {
     if (op->prof_used >= op->prof_events.size()) {
       cudaEvent_t s0, s1;
       CU_TRY(cudaEventCreate(&s0));
@@ -272,7 +280,7 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   }
   CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
   op->launches++;
-  if (op->profiling) CU_TRY(record_event(e_stop, st));
+  if (timed) CU_TRY(record_event(e_stop, st));
   return HB_OK;
 }
 
@@ -330,28 +338,32 @@ int nccl_assembly_exchange(hb_op* op, cudaStream_t cs) {
 }
 
 // y = A x for one op (P = 1, or P > 1 with NCCL).  init_y=false: y already holds the
-// assembly initialisation (lambda x or 0), as written by the CG p-update.
-int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStream_t st) {
+// assembly initialisation (lambda x or 0), as written by the CG p-update.  energy=true (CG):
+// the operator launches also reduce p.Ap (element energy) into the CG scalars.
+int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStream_t st, bool energy = false) {
   const int64_t E = op->sz.E_local;
   const bool multi = op->comm && op->comm->P > 1;
   if (!multi) {
     HB_TRY(stage_init(op, x, y, init_y, st));
-    return launch_ax(op, op->ax_plain, 0, E, x, y, st);
+    return launch_ax(op, op->ax_plain, 0, E, x, y, st, energy, true);
   }
+  // the last non-empty launch publishes p.Ap
+  const int64_t nA = op->nA, nH = op->nH, nB = E - nA - nH;
+  const int last = nB > 0 ? 2 : (nH > 0 ? 1 : 0);
   cudaStream_t cs = op->comm_stream;
   HB_TRY(stage_init(op, x, y, init_y, st));
   CU_TRY(cudaEventRecord(op->ev_pack, st));
   CU_TRY(cudaStreamWaitEvent(cs, op->ev_pack, 0));
   HB_TRY(nccl_halo_exchange(op, cs));
   CU_TRY(cudaEventRecord(op->ev_halo, cs));
-  HB_TRY(launch_ax(op, op->ax_plain, 0, op->nA, x, y, st));                          // interior A
+  HB_TRY(launch_ax(op, op->ax_plain, 0, nA, x, y, st, energy, last == 0));                      // interior A
   CU_TRY(cudaStreamWaitEvent(st, op->ev_halo, 0));
-  HB_TRY(launch_ax(op, op->ax_halo, op->nA, op->nA + op->nH, x, y, st));             // halo elements
+  HB_TRY(launch_ax(op, op->ax_halo, nA, nA + nH, x, y, st, energy, last == 1));                 // halo elements
   CU_TRY(cudaEventRecord(op->ev_haloel, st));
   CU_TRY(cudaStreamWaitEvent(cs, op->ev_haloel, 0));
   HB_TRY(nccl_assembly_exchange(op, cs));
   CU_TRY(cudaEventRecord(op->ev_gather, cs));
-  HB_TRY(launch_ax(op, op->ax_plain, op->nA + op->nH, E, x, y, st));                 // interior B
+  HB_TRY(launch_ax(op, op->ax_plain, nA + nH, E, x, y, st, energy, last == 2));                 // interior B
   CU_TRY(cudaStreamWaitEvent(st, op->ev_gather, 0));
   return stage_unpack(op, y, st);
 }
@@ -402,6 +414,24 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     double Dp[256] = {0};
     for (int t = 0; t < NP * NP; ++t) Dp[t] = m->D[t];
     CU_TRY(cudaMemcpyToSymbol(hbk::c_D, Dp, sizeof(Dp), sizeof(double) * 256 * N));
+    // even/odd folded D and D^T for the line-owner kernel (ax_lines.cuh): rows padded to even
+    // length; Me[i][m] = (M[i][m] + M[i][N-m]) / 2 (m < H), M[i][H] (middle column, odd N+1);
+    // Mo[i][m] = (M[i][m] - M[i][N-m]) / 2; middle row M[H][m] (odd N+1)
+    const int H = NP / 2, odd = NP & 1, HE = H + odd, HE2 = HE + (HE & 1), H2 = H + (H & 1);
+    const int MAT = H * HE2 + H * H2 + H2;
+    std::vector<double> eo(hbk::EO_MAX, 0.0);
+    for (int tr = 0; tr < 2; ++tr) {
+      auto M = [&](int i, int mm) { return tr ? m->D[mm * NP + i] : m->D[i * NP + mm]; };
+      double* o = eo.data() + tr * MAT;
+      for (int i = 0; i < H; ++i) {
+        for (int mm = 0; mm < H; ++mm) o[i * HE2 + mm] = 0.5 * (M(i, mm) + M(i, N - mm));
+        if (odd) o[i * HE2 + H] = M(i, H);
+        for (int mm = 0; mm < H; ++mm) o[H * HE2 + i * H2 + mm] = 0.5 * (M(i, mm) - M(i, N - mm));
+      }
+      if (odd)
+        for (int mm = 0; mm < H; ++mm) o[H * HE2 + H * H2 + mm] = M(H, mm);
+    }
+    CU_TRY(cudaMemcpyToSymbol(hbk::g_EO, eo.data(), sizeof(double) * hbk::EO_MAX, sizeof(double) * hbk::EO_MAX * N));
   }
   HB_TRY(op->idx.alloc(NL * sizeof(int32_t)));
   CU_TRY(cudaMemcpyAsync(op->idx.p, m->idx.data(), NL * sizeof(int32_t), cudaMemcpyHostToDevice, st));
@@ -472,6 +502,7 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k->fn, k->block, k->smem));
     k->grid_max = std::max(1, nb) * num_sms();
   }
+  HB_TRY(op->e_part.alloc((size_t)std::max(op->ax_plain.grid_max, op->ax_halo.grid_max) * 8 + 64));
   if (m->P > 1 && comm) {
     int lo, hi;
     CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -559,14 +590,11 @@ int cg_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
   return allreduce_sum(op, &s->rr_new, st);
 }
 
-// One CG iteration after the operator: dot, x/r update, optionally the p update.
+// One CG iteration after the operator (which published p.Ap): x/r update + r.r, then p update.
 int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   const int64_t n = op->sz.n_owned;
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
   const int gv = vec_grid(std::max<int64_t>(n, 1));
-  hbk::cg_dot_pAp<<<gv, hbk::VEC_BLOCK, 0, st>>>(op->p.as<double>(), op->Ap.as<double>(), n,
-                                                 op->partials.as<double>(), s, op->hist.as<double>());
-  op->launches++;
   HB_TRY(allreduce_sum(op, &s->pAp, st));
   hbk::cg_update_xr<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n,
                                                    op->partials.as<double>(), s);
@@ -579,14 +607,15 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
 int cg_vec_part2(hb_op* op, cudaStream_t st) {
   const int64_t n = op->sz.n_owned;
   hbk::cg_update_p<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
-      op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n, lam_init(op), op->scal.as<hbk::CgScalars>());
+      op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n, lam_init(op), op->partials.as<double>(),
+      op->scal.as<hbk::CgScalars>());
   op->launches++;
   CU_TRY(cudaGetLastError());
   return HB_OK;
 }
 
 int cg_iteration(hb_op* op, double* x, cudaStream_t st) {
-  HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st));
+  HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
   HB_TRY(cg_vec_part1(op, x, st));
   return cg_vec_part2(op, st);
 }
@@ -622,7 +651,7 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
   HB_TRY(ensure_hist(op, K));
   hb_op::GraphKey key{K, b, x, op->profiling, st};
   auto it = op->graphs.find(key);
-  if (op->profiling) op->prof_used = 0;  // a profiling graph records into events 0..n-1
+  if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; }  // a profiling graph records into events 0..n-1
   if (it == op->graphs.end()) {
     int64_t l0 = op->launches;
     cudaGraph_t graph;
@@ -656,7 +685,7 @@ int cg_tol(hb_op* op, const double* b, double* x, int32_t max_iters, double eps,
   int32_t j = 0;
   double rr = hs->rr_new;
   while (j < max_iters && rr > eps) {
-    HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st));
+    HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
     HB_TRY(cg_vec_part1(op, x, st));
     CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaStreamSynchronize(st));
@@ -699,10 +728,16 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
 }
 
 extern "C" int hb_op_set_profiling(hb_op* op, int enable) {
-  if (!op) { set_error("hb_op_set_profiling: null pointer"); return HB_ERR_ARG; }
-  if ((bool)enable != op->profiling) {
-    op->profiling = enable != 0;
+  if (!op || enable < 0) { set_error("hb_op_set_profiling: bad argument"); return HB_ERR_ARG; }
+  const bool on = enable != 0;
+  if (on != op->profiling || (on && enable != op->prof_stride)) {
+    // captured graphs bake the event pattern in: drop them when it changes
+    for (auto& kv : op->graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->graphs.clear();
   }
+  op->profiling = on;
+  op->prof_stride = on ? enable : 1;
+  op->prof_seq = 0;
   op->prof_used = 0;
   return HB_OK;
 }
@@ -809,19 +844,27 @@ int group_assembly_exchange(hb_group* g, cudaStream_t st) {
   return HB_OK;
 }
 
-int group_apply_internal(hb_group* g, const double* const* x, double* const* y, bool init_y, cudaStream_t st) {
+int group_apply_internal(hb_group* g, const double* const* x, double* const* y, bool init_y, cudaStream_t st,
+                         bool energy = false) {
   const size_t P = g->ops.size();
+  auto last_of = [](hb_op* a) {
+    const int64_t nB = a->sz.E_local - a->nA - a->nH;
+    return nB > 0 ? 2 : (a->nH > 0 ? 1 : 0);
+  };
   for (size_t r = 0; r < P; ++r) HB_TRY(stage_init(g->ops[r], x[r], y[r], init_y, st));
   HB_TRY(group_halo_exchange(g, st));
-  for (size_t r = 0; r < P; ++r) HB_TRY(launch_ax(g->ops[r], g->ops[r]->ax_plain, 0, g->ops[r]->nA, x[r], y[r], st));
   for (size_t r = 0; r < P; ++r) {
     hb_op* a = g->ops[r];
-    HB_TRY(launch_ax(a, a->ax_halo, a->nA, a->nA + a->nH, x[r], y[r], st));
+    HB_TRY(launch_ax(a, a->ax_plain, 0, a->nA, x[r], y[r], st, energy, last_of(a) == 0));
+  }
+  for (size_t r = 0; r < P; ++r) {
+    hb_op* a = g->ops[r];
+    HB_TRY(launch_ax(a, a->ax_halo, a->nA, a->nA + a->nH, x[r], y[r], st, energy, last_of(a) == 1));
   }
   HB_TRY(group_assembly_exchange(g, st));
   for (size_t r = 0; r < P; ++r) {
     hb_op* a = g->ops[r];
-    HB_TRY(launch_ax(a, a->ax_plain, a->nA + a->nH, a->sz.E_local, x[r], y[r], st));
+    HB_TRY(launch_ax(a, a->ax_plain, a->nA + a->nH, a->sz.E_local, x[r], y[r], st, energy, last_of(a) == 2));
   }
   for (size_t r = 0; r < P; ++r) HB_TRY(stage_unpack(g->ops[r], y[r], st));
   return HB_OK;
@@ -875,13 +918,7 @@ extern "C" int hb_group_cg_solve(hb_group* g, const double* const* b, double* co
   std::vector<double*> av(P);
   for (int r = 0; r < P; ++r) { pv[r] = g->ops[r]->p.as<double>(); av[r] = g->ops[r]->Ap.as<double>(); }
   while (j < max_iters && (eps < 0 || rr > eps)) {
-    HB_TRY(group_apply_internal(g, pv.data(), av.data(), false, st));
-    for (int r = 0; r < P; ++r) {
-      hb_op* a = g->ops[r];
-      const int64_t n = a->sz.n_owned;
-      hbk::cg_dot_pAp<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
-          a->p.as<double>(), a->Ap.as<double>(), n, a->partials.as<double>(), a->scal.as<hbk::CgScalars>(), a->hist.as<double>());
-    }
+    HB_TRY(group_apply_internal(g, pv.data(), av.data(), false, st, true));
     HB_TRY(group_allreduce(g, off_pAp, st));
     for (int r = 0; r < P; ++r) {
       hb_op* a = g->ops[r];

@@ -1,7 +1,8 @@
 // CG vector kernels (K4 of SURVEY §2C): fused, vectorised, deterministic.
 //
-// Alg. 1 with the paper's fusions: p.Ap in its own reduction kernel;
-// r -= alpha Ap fused with r.r; x += alpha p; p = r + beta p.  alpha and beta never leave
+// Alg. 1 with the paper's fusions: r -= alpha Ap fused with r.r, and
+// x += alpha p; p = r + beta p (fused with p.p).  The paper's separate p.Ap kernel is folded
+// into the operator as the element energy (ax_lines.cuh energy_finish).  alpha and beta never leave
 // the device: every kernel reads the reduced scalars from CgScalars and computes them
 // itself, so an iteration has no host round trip and can be captured in a CUDA graph.
 // Reductions: fp64 per thread -> warp shuffle -> CTA -> one partial per CTA; the last CTA
@@ -10,17 +11,9 @@
 #pragma once
 #include <cstdint>
 
-namespace hbk {
+#include "common.cuh"  // CgScalars
 
-struct CgScalars {
-  double pAp;      // p.Ap (global after allreduce)
-  double rr;       // r_j.r_j
-  double rr_new;   // r_{j+1}.r_{j+1} (global after allreduce)
-  double pad;
-  int32_t it;      // iteration counter j
-  uint32_t ticket; // last-CTA detection
-  int32_t pad2[2];
-};
+namespace hbk {
 
 constexpr int VEC_BLOCK = 256;
 
@@ -83,30 +76,10 @@ cg_init(const double* __restrict__ b, double* __restrict__ x, double* __restrict
   }
   double tot;
   if (finish_reduction(acc, partials, &s->ticket, &tot)) {
-    s->rr_new = tot;
+    s->rr_new = tot;  // allreduced for P > 1
+    s->pp = tot;      // local p.p (p = r)
+    s->e_acc = 0.0;
     s->it = 0;
-  }
-}
-
-// p.Ap; the last CTA also rotates rr <- rr_new and records the history
-__global__ void __launch_bounds__(VEC_BLOCK)
-cg_dot_pAp(const double* __restrict__ p, const double* __restrict__ Ap, int64_t n,
-           double* partials, CgScalars* s, double* hist) {
-  double acc = 0.0;
-  const int64_t n2 = n >> 1;
-  const double2* p2 = reinterpret_cast<const double2*>(p);
-  const double2* a2 = reinterpret_cast<const double2*>(Ap);
-  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
-    double2 pv = p2[l], av = a2[l];
-    acc = fma(pv.x, av.x, acc);
-    acc = fma(pv.y, av.y, acc);
-  }
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) acc = fma(p[n - 1], Ap[n - 1], acc);
-  double tot;
-  if (finish_reduction(acc, partials, &s->ticket, &tot)) {
-    s->pAp = tot;
-    s->rr = s->rr_new;
-    if (hist) hist[s->it] = s->rr_new;
   }
 }
 
@@ -140,12 +113,14 @@ cg_update_xr(double* __restrict__ x, const double* __restrict__ p, double* __res
   if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_new = tot;
 }
 
-// beta = rr_new / rr;  p = r + beta p;  Ap = lam_init p (assembly init of the next apply)
+// beta = rr_new / rr;  p = r + beta p;  Ap = lam_init p (assembly init of the next apply);
+// partial p.p -> pp (lambda term of the next fused p.Ap); j += 1
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_p(double* __restrict__ p, const double* __restrict__ r, double* __restrict__ Ap,
-            int64_t n, double lam_init, CgScalars* s) {
+            int64_t n, double lam_init, double* partials, CgScalars* s) {
   const double rr = s->rr;
   const double beta = (rr != 0.0) ? s->rr_new / rr : 0.0;  // c15 guard
+  double acc = 0.0;
   const int64_t n2 = n >> 1;
   double2* p2 = reinterpret_cast<double2*>(p);
   const double2* r2 = reinterpret_cast<const double2*>(r);
@@ -155,13 +130,19 @@ cg_update_p(double* __restrict__ p, const double* __restrict__ r, double* __rest
     pv.x = fma(beta, pv.x, rv.x); pv.y = fma(beta, pv.y, rv.y);
     p2[l] = pv;
     a2[l] = make_double2(lam_init * pv.x, lam_init * pv.y);
+    acc = fma(pv.x, pv.x, acc); acc = fma(pv.y, pv.y, acc);
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t l = n - 1;
     double pv = fma(beta, p[l], r[l]);
     p[l] = pv; Ap[l] = lam_init * pv;
+    acc = fma(pv, pv, acc);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) s->it += 1;
+  double tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) {
+    s->pp = tot;
+    s->it += 1;
+  }
 }
 
 // generic dot a.b -> *out (used by hb_dot)

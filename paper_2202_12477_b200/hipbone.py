@@ -298,8 +298,9 @@ class Operator:
                                      _ptr(h, C.c_double) if hist else None, C.byref(res), _stream(stream)))
         return res.iterations, (h[:res.iterations + 1].copy() if hist else None)
 
-    def set_profiling(self, enable: bool):
-        _check(_lib.hb_op_set_profiling(self._h, int(enable)))
+    def set_profiling(self, enable, stride: int = 1):
+        """enable=False: off; else time every `stride`-th operator launch with CUDA events."""
+        _check(_lib.hb_op_set_profiling(self._h, int(stride) if enable else 0))
 
     def kernel_time(self):
         n = C.c_int64()

@@ -308,3 +308,38 @@ def _w_row(row, box, N):
 def test_stream_bench_runs(hb):
     v = hb.stream_bench(1 << 22, 5)
     assert np.isfinite(v) and v > 1e11
+
+
+@pytest.mark.parametrize("N,mass_mode", [(4, 1), (7, 0), (2, 1)])
+def test_cg_random_geometry_both_mass_modes(hb, N, mass_mode):
+    """CG with random SPD geometric factors (cross terms live) and both mass modes: the
+    fused p.Ap (element energy + lambda p.p, or + lambda u.B u in mode 1) must give the
+    oracle's Alg. 1 iterates (c18)."""
+    box = (3, 2, 3)
+    E = int(np.prod(box))
+    # geometry scaled by the GLL weight products like the real factors (SURVEY §8(d)), so the
+    # problem is as well conditioned as the benchmark's and CG is not in the roundoff regime
+    xg, w = basis.gll(N)
+    wq = np.einsum("k,j,i->kji", w, w, w).ravel()
+    G = random_spd_factors(E, (N + 1) ** 3, seed=31 + N, scale=wq)
+    B = random_positive((E, (N + 1) ** 3), 77) if mass_mode == 1 else None
+    o = OracleProblem(box, N, mass_mode=mass_mode, G=G, B=B)
+    A = lambda v: o.apply(v, 1.0)
+    bo = of.forcing(range(o.NG), 1)
+    eps = 1e-16 * ocg.dot(bo, bo)
+    xo, jo, ho = ocg.cg(A, bo, max_iters=300, eps=eps)
+    m = hb.Mesh(*box, N, mass_mode=mass_mode)
+    m.set_geometry(G)
+    if B is not None:
+        m.set_mass(B)
+    op = hb.Operator(m)
+    b = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.forcing(1, b)
+    x = torch.zeros_like(b)
+    jg, hg = op.cg(b, x, 300, eps)
+    assert jg == jo and jo < 100
+    _cg_contract(hg, ho, jo - 1)
+    assert np.abs(x.cpu().numpy() - xo).max() <= 1e-10 * np.abs(xo).max()
+    x = torch.zeros_like(b)
+    jf, hf = op.cg(b, x, jo)  # fixed mode, graph path
+    _cg_contract(hf, ho, jo - 1)
