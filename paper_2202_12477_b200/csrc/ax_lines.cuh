@@ -64,9 +64,9 @@ struct LinesShape {
   static constexpr int CONST = 2 * MAT;               // D and D^T (host-built, g_EO[N])
   static_assert(CONST <= EO_MAX, "folded D table");
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
-  // resident CTAs per SM requested from ptxas: ~96 (N <= 7) / 128 registers per thread
+  // resident CTAs per SM requested from ptxas: ~96 (N <= 6) / 128 registers per thread
   // (enough for the line arrays), capped by the shared-memory footprint and 32 CTAs/SM
-  static constexpr int REGS = N <= 7 ? 96 : 128;
+  static constexpr int REGS = N <= 6 ? 96 : 128;
   static constexpr int MINB_REG0 = 65536 / (BLOCK * REGS);
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));

@@ -104,9 +104,8 @@ AxKernel pick_ax_n(bool halo, bool massb) {
 // experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
 AxKernel pick_ax_variant(int v) {
   switch (v) {
-    case 1: return make_lines<7, false, false, 0, 10, 0, false>();  // no per-element L2 prefetch
-    case 2: return make_lines<7, false, false, 0, 8, 1>();          // 128 regs
-    case 3: return make_lines<7, false, false, 0, 12, 1>();         // 80 regs
+    case 1: return make_lines<7, false, false, 0, 10, 1>();         // 96 regs
+    case 2: return make_lines<7, false, false, 0, 8, 1, false>();   // no L2 prefetch of G
     default: return make_lines<7, false, false, kLinesPF>();
   }
 }
@@ -596,10 +595,25 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
   const int gv = vec_grid(std::max<int64_t>(n, 1));
   HB_TRY(allreduce_sum(op, &s->pAp, st));
-  hbk::cg_update_xr<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n,
-                                                   op->partials.as<double>(), s);
+  if (!op->comm || op->comm->P == 1) {  // one GPU: x and r updates fused in one pass
+    hbk::cg_update_xr<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(),
+                                                     n, op->partials.as<double>(), s);
+    op->launches++;
+    CU_TRY(cudaGetLastError());
+    return HB_OK;
+  }
+  // P > 1: r update + r.r, then the r.r allreduce on the comm stream overlapped with
+  // the x AXPY on the compute stream
+  hbk::cg_update_r<<<gv, hbk::VEC_BLOCK, 0, st>>>(op->r.as<double>(), op->Ap.as<double>(), n,
+                                                  op->partials.as<double>(), s);
   op->launches++;
-  HB_TRY(allreduce_sum(op, &s->rr_new, st));
+  CU_TRY(cudaEventRecord(op->ev_red, st));
+  CU_TRY(cudaStreamWaitEvent(op->comm_stream, op->ev_red, 0));
+  NC_TRY(ncclAllReduce(&s->rr_new, &s->rr_new, 1, ncclFloat64, ncclSum, op->comm->nccl, op->comm_stream));
+  CU_TRY(cudaEventRecord(op->ev_red_done, op->comm_stream));
+  hbk::cg_update_x<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), n, s);
+  op->launches++;
+  CU_TRY(cudaStreamWaitEvent(st, op->ev_red_done, 0));
   CU_TRY(cudaGetLastError());
   return HB_OK;
 }
@@ -920,13 +934,19 @@ extern "C" int hb_group_cg_solve(hb_group* g, const double* const* b, double* co
   while (j < max_iters && (eps < 0 || rr > eps)) {
     HB_TRY(group_apply_internal(g, pv.data(), av.data(), false, st, true));
     HB_TRY(group_allreduce(g, off_pAp, st));
+    for (int r = 0; r < P; ++r) {  // same split as the NCCL path: r update + r.r, then x AXPY
+      hb_op* a = g->ops[r];
+      const int64_t n = a->sz.n_owned;
+      hbk::cg_update_r<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+          a->r.as<double>(), a->Ap.as<double>(), n, a->partials.as<double>(), a->scal.as<hbk::CgScalars>());
+    }
+    HB_TRY(group_allreduce(g, off_rrn, st));
     for (int r = 0; r < P; ++r) {
       hb_op* a = g->ops[r];
       const int64_t n = a->sz.n_owned;
-      hbk::cg_update_xr<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
-          x[r], a->p.as<double>(), a->r.as<double>(), a->Ap.as<double>(), n, a->partials.as<double>(), a->scal.as<hbk::CgScalars>());
+      hbk::cg_update_x<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+          x[r], a->p.as<double>(), n, a->scal.as<hbk::CgScalars>());
     }
-    HB_TRY(group_allreduce(g, off_rrn, st));
     if (eps >= 0) {
       HB_TRY(read0());
       if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_new)) {

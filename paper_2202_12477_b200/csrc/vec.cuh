@@ -113,6 +113,47 @@ cg_update_xr(double* __restrict__ x, const double* __restrict__ p, double* __res
   if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_new = tot;
 }
 
+// Split form used with P > 1: r -= alpha Ap with r.r first, so the r.r allreduce can
+// run on the communication stream while x += alpha p executes ("hidden behind the AXPY").
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_update_r(double* __restrict__ r, const double* __restrict__ Ap, int64_t n, double* partials, CgScalars* s) {
+  const double pAp = s->pAp;
+  const double alpha = (pAp != 0.0) ? s->rr / pAp : 0.0;  // c15 guard
+  double acc = 0.0;
+  const int64_t n2 = n >> 1;
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* a2 = reinterpret_cast<const double2*>(Ap);
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double2 rv = r2[l], av = a2[l];
+    rv.x = fma(-alpha, av.x, rv.x); rv.y = fma(-alpha, av.y, rv.y);
+    r2[l] = rv;
+    acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    double rv = fma(-alpha, Ap[l], r[l]);
+    r[l] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  double tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_new = tot;
+}
+
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_update_x(double* __restrict__ x, const double* __restrict__ p, int64_t n, const CgScalars* s) {
+  const double pAp = s->pAp;
+  const double alpha = (pAp != 0.0) ? s->rr / pAp : 0.0;
+  const int64_t n2 = n >> 1;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    double2 xv = x2[l], pv = p2[l];
+    xv.x = fma(alpha, pv.x, xv.x); xv.y = fma(alpha, pv.y, xv.y);
+    x2[l] = xv;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) x[n - 1] = fma(alpha, p[n - 1], x[n - 1]);
+}
+
 // beta = rr_new / rr;  p = r + beta p;  Ap = lam_init p (assembly init of the next apply);
 // partial p.p -> pp (lambda term of the next fused p.Ap); j += 1
 __global__ void __launch_bounds__(VEC_BLOCK)
