@@ -151,6 +151,10 @@ __device__ __forceinline__ void energy_finish(double en, const AxArgs& a, double
     if (t < h && t + h < BLOCK) red[t] += red[t + h];
     __syncthreads();
   }
+  if (a.e_final == 2) {  // deferred: cg_update_xr_e sums the partials
+    if (t == 0) a.e_part[blockIdx.x] = red[0];
+    return;
+  }
   if (t == 0) {
     a.e_part[blockIdx.x] = red[0];
     __threadfence();

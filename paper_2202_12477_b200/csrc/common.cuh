@@ -41,7 +41,9 @@ struct AxArgs {
   double* e_part;   // per-CTA partial energies
   double* hist;     // r.r history (written with the rr rotation by the final launch)
   double lam_pp;    // lambda (mass mode 0) or 0 (mode 1: lambda B is in the element energy)
-  int32_t e_final;  // this launch completes the apply: publish p.Ap
+  int32_t e_final;  // 0: accumulate into e_acc; 1: this launch completes the apply, publish
+                    // p.Ap; 2: single-launch apply (P = 1): only write the per-CTA partials,
+                    // the x/r update kernel reduces them (no fence/atomic in the operator)
 };
 
 template <bool HALO>

@@ -196,6 +196,7 @@ struct hb_op {
   std::vector<int32_t> nbr;
   std::vector<int64_t> soff, scnt, roff, rcnt;
   int64_t n_send = 0;
+  int last_grid = 0;  // grid of the last operator launch (number of energy partials, P = 1)
   AxKernel ax_plain, ax_halo;
   cudaStream_t comm_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture (the legacy stream cannot be captured)
@@ -259,9 +260,10 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.e_part = op->e_part.as<double>();
   a.hist = op->hist.as<double>();
   a.lam_pp = op->mass_mode == 0 ? op->lam : 0.0;
-  a.e_final = final_launch ? 1 : 0;
+  a.e_final = final_launch ? ((op->comm && op->comm->P > 1) || op->grouped ? 1 : 2) : 0;
   int64_t groups = (e1 - e0 + k.epb - 1) / k.epb;
   int grid = (int)std::min<int64_t>(groups, (int64_t)k.grid_max);
+  if (energy && final_launch) op->last_grid = grid;
   void* args[] = {&a};
   cudaEvent_t e_start = nullptr, e_stop = nullptr;
   const bool timed = op->profiling && (op->prof_seq++ % op->prof_stride == 0);
@@ -577,6 +579,7 @@ extern "C" int hb_dot(hb_op* op, const double* a, const double* b, double* out_h
 namespace {
 
 double lam_init(const hb_op* op) { return op->mass_mode == 0 ? op->lam : 0.0; }
+double lam_pp(const hb_op* op) { return op->mass_mode == 0 ? op->lam : 0.0; }
 
 int cg_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
   const int64_t n = op->sz.n_owned;
@@ -595,9 +598,10 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
   const int gv = vec_grid(std::max<int64_t>(n, 1));
   HB_TRY(allreduce_sum(op, &s->pAp, st));
-  if (!op->comm || op->comm->P == 1) {  // one GPU: x and r updates fused in one pass
-    hbk::cg_update_xr<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(),
-                                                     n, op->partials.as<double>(), s);
+  if (!op->comm || op->comm->P == 1) {  // one GPU: energy reduction + x and r updates in one pass
+    hbk::cg_update_xr_e<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(),
+                                                       n, op->e_part.as<double>(), op->last_grid, lam_pp(op),
+                                                       op->partials.as<double>(), s, op->hist.as<double>());
     op->launches++;
     CU_TRY(cudaGetLastError());
     return HB_OK;
