@@ -236,18 +236,21 @@ def main():
     # ---- timed region: K steps, device-timed with events, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     op_times = []
+    phases = []
     l0 = op.launch_count()
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         for t in range(args.steps):
+            hb.l2_reset()   # persisting lines back to normal, then flush: every step starts cold
             flush.zero_()
             ev[t][0].record(stream)
             step()
             ev[t][1].record(stream)
             if not args.no_profile:
                 op_times.append(op.kernel_time())  # synchronises on this step's last op event
+                phases.append(op.phase_times())
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -274,6 +277,7 @@ def main():
         dist.barrier()
     e2e_ms = []
     for t in range(args.steps):
+        hb.l2_reset()
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -318,7 +322,8 @@ def main():
                                       + (f" (C4-shaped weak scaling, {blk[0]}x{blk[1]}x{blk[2]} per GPU)" if world > 1 else ""),
                           "box": list(box), "N": N, "E": E_glob, "N_G": NG, "N_L": E_glob * (N + 1) ** 3,
                           "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
-                          "l2": "flushed between steps (256 MiB write); working set > L2",
+                          "l2": "flushed between steps (persisting lines reset + 256 MiB write); working set > L2",
+                          "l2_resident_bytes": op.l2_resident_bytes(),
                           "parallelism": f"element partition p{world}"},
                "gdofs_per_s": round(gdofs, 4),
                "cg_bytes_per_iter_fused": ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3),
@@ -326,6 +331,10 @@ def main():
                "e2e": {"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
                        "d2h_bytes_per_step": 8 * n + 48},
                "gpu_launches": launches,
+               "phase_ms_per_iter": ({"operator": round(1e3 * sum(p[0] for p in phases) / len(phases), 4),
+                                      "xr_update": round(1e3 * sum(p[1] for p in phases) / len(phases), 4),
+                                      "p_update": round(1e3 * sum(p[2] for p in phases) / len(phases), 4)}
+                                     if phases else None),
                "roofline": roof,
                "cpu_baseline": cpu,
                "clocks": clk.summary()}

@@ -65,14 +65,21 @@ namespace {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  ~DevBuf() { if (p) cudaFree(p); }
+  bool own = true;
+  ~DevBuf() { if (p && own) cudaFree(p); }
   int alloc(size_t b) {
-    if (p) { cudaFree(p); p = nullptr; }
+    if (p && own) cudaFree(p);
+    p = nullptr;
+    own = true;
     bytes = b;
     if (b == 0) return HB_OK;
     cudaError_t e = cudaMalloc(&p, b);
     if (e != cudaSuccess) { p = nullptr; set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e)); return HB_ERR_OOM; }
     return HB_OK;
+  }
+  void view(void* ptr, size_t b) {  // non-owning sub-range of an arena
+    if (p && own) cudaFree(p);
+    p = ptr; bytes = b; own = false;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
@@ -175,7 +182,7 @@ int num_sms() {
 
 int vec_grid(int64_t n) {
   int64_t need = (n / 2 + hbk::VEC_BLOCK - 1) / hbk::VEC_BLOCK;
-  int64_t cap = (int64_t)num_sms() * 8;
+  int64_t cap = (int64_t)num_sms() * 2;  // 2 x 512-thread CTAs per SM: few partials, cheap last-CTA tickets
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
 }
 
@@ -190,6 +197,8 @@ struct hb_op {
   bool grouped = false;
   int64_t nA = 0, nH = 0, nB = 0;
   // device data
+  DevBuf arena;  // [idx | r | p | Ap | xs]: the data re-read every CG iteration, one L2 window
+  size_t l2_window = 0;  // bytes of the arena marked L2-persisting for the captured CG graph
   DevBuf idx, G, B, owned_gid;
   DevBuf r, p, Ap, xs, partials, e_part, scal, hist, dot_out, dot_ticket;
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
@@ -209,6 +218,11 @@ struct hb_op {
   int64_t prof_seq = 0;     // operator launches seen since profiling was (re)enabled
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
+  bool last_timed = false;  // the last operator launch was timed: time this iteration's vector kernels too
+  struct Timer {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+  } t_xr, t_p;  // CG vector phases (x/r update, p update)
   int64_t launches = 0;
   // fixed-mode graph cache
   struct GraphKey {
@@ -217,12 +231,14 @@ struct hb_op {
       return std::tie(K, b, x, prof, st) < std::tie(o.K, o.b, o.x, o.prof, o.st);
     }
   };
-  struct GraphVal { cudaGraphExec_t exec; int64_t launches; size_t prof_events; };
+  struct GraphVal { cudaGraphExec_t exec; int64_t launches; size_t prof_events, prof_xr, prof_p; };
   std::map<GraphKey, GraphVal> graphs;
   double* host_scal = nullptr;  // pinned CgScalars mirror
   ~hb_op() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto& pr : prof_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (Timer* tm : {&t_xr, &t_p})
+      for (auto& pr : tm->ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (ev_cap) cudaEventDestroy(ev_cap);
@@ -267,6 +283,7 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   void* args[] = {&a};
   cudaEvent_t e_start = nullptr, e_stop = nullptr;
   const bool timed = op->profiling && (op->prof_seq++ % op->prof_stride == 0);
+  op->last_timed = timed;
   if (timed) {
     if (op->prof_used >= op->prof_events.size()) {
       cudaEvent_t s0, s1;
@@ -282,6 +299,24 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
   op->launches++;
   if (timed) CU_TRY(record_event(e_stop, st));
+  return HB_OK;
+}
+
+// bracket a vector phase with events when the iteration's operator launch was timed
+int phase_event(hb_op* op, hb_op::Timer& tm, bool start, cudaStream_t st) {
+  if (!op->last_timed) return HB_OK;
+  if (start) {
+    if (tm.used >= tm.ev.size()) {
+      cudaEvent_t s0, s1;
+      CU_TRY(cudaEventCreate(&s0));
+      CU_TRY(cudaEventCreate(&s1));
+      tm.ev.push_back({s0, s1});
+    }
+    CU_TRY(record_event(tm.ev[tm.used].first, st));
+  } else {
+    CU_TRY(record_event(tm.ev[tm.used].second, st));
+    tm.used++;
+  }
   return HB_OK;
 }
 
@@ -434,7 +469,18 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     }
     CU_TRY(cudaMemcpyToSymbol(hbk::g_EO, eo.data(), sizeof(double) * hbk::EO_MAX, sizeof(double) * hbk::EO_MAX * N));
   }
-  HB_TRY(op->idx.alloc(NL * sizeof(int32_t)));
+  // arena of everything a CG iteration re-reads besides G (candidates for L2 residency)
+  {
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t bi = al(NL * sizeof(int32_t)), bv = al((size_t)std::max<int64_t>(n, 1) * 8);
+    HB_TRY(op->arena.alloc(bi + 4 * bv));
+    char* base = op->arena.as<char>();
+    op->idx.view(base, NL * sizeof(int32_t));
+    op->r.view(base + bi, bv);
+    op->p.view(base + bi + bv, bv);
+    op->Ap.view(base + bi + 2 * bv, bv);
+    op->xs.view(base + bi + 3 * bv, bv);
+  }
   CU_TRY(cudaMemcpyAsync(op->idx.p, m->idx.data(), NL * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   HB_TRY(op->G.alloc(NL * 6 * sizeof(double)));
   if (m->has_G) {
@@ -465,10 +511,6 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     CU_TRY(cudaMemcpyAsync(op->owned_gid.p, m->owned.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   }
   // CG workspace
-  HB_TRY(op->r.alloc(std::max<int64_t>(n, 1) * 8));
-  HB_TRY(op->p.alloc(std::max<int64_t>(n, 1) * 8));
-  HB_TRY(op->Ap.alloc(std::max<int64_t>(n, 1) * 8));
-  HB_TRY(op->xs.alloc(std::max<int64_t>(n, 1) * 8));
   HB_TRY(op->partials.alloc((size_t)num_sms() * 8 * 8 + 64));
   HB_TRY(op->scal.alloc(sizeof(hbk::CgScalars)));
   CU_TRY(cudaMemsetAsync(op->scal.p, 0, sizeof(hbk::CgScalars), st));
@@ -510,6 +552,30 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     CU_TRY(cudaStreamCreateWithPriority(&op->comm_stream, cudaStreamNonBlocking, hi));
   }
   CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
+  // L2 residency (B200: 126 MB L2): when the arena fits the persisting-L2 budget, kernels
+  // captured from cap_stream (the fixed-iteration CG graph) keep idx and the CG vectors
+  // L2-resident across iterations while G streams from HBM.  HB_L2_PERSIST=0 disables.
+  {
+    const char* env = getenv("HB_L2_PERSIST");
+    int dev = 0, maxp = 0, maxw = 0;
+    CU_TRY(cudaGetDevice(&dev));
+    CU_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    CU_TRY(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    const size_t want = op->arena.bytes;
+    if (!(env && env[0] == '0') && want > 0 && want <= (size_t)maxp && want <= (size_t)maxw) {
+      size_t cur = 0;
+      CU_TRY(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+      if (cur < want) CU_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.base_ptr = op->arena.p;
+      v.accessPolicyWindow.num_bytes = want;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      CU_TRY(cudaStreamSetAttribute(op->cap_stream, cudaStreamAttributeAccessPolicyWindow, &v));
+      op->l2_window = want;
+    }
+  }
   for (cudaEvent_t* e : {&op->ev_pack, &op->ev_halo, &op->ev_haloel, &op->ev_gather, &op->ev_red, &op->ev_red_done, &op->ev_cap})
     CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CU_TRY(cudaStreamSynchronize(st));
@@ -599,12 +665,13 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   const int gv = vec_grid(std::max<int64_t>(n, 1));
   HB_TRY(allreduce_sum(op, &s->pAp, st));
   if (!op->comm || op->comm->P == 1) {  // one GPU: energy reduction + x and r updates in one pass
+    HB_TRY(phase_event(op, op->t_xr, true, st));
     hbk::cg_update_xr_e<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(),
                                                        n, op->e_part.as<double>(), op->last_grid, lam_pp(op),
                                                        op->partials.as<double>(), s, op->hist.as<double>());
     op->launches++;
     CU_TRY(cudaGetLastError());
-    return HB_OK;
+    return phase_event(op, op->t_xr, false, st);
   }
   // P > 1: r update + r.r, then the r.r allreduce on the comm stream overlapped with
   // the x AXPY on the compute stream
@@ -624,11 +691,14 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
 
 int cg_vec_part2(hb_op* op, cudaStream_t st) {
   const int64_t n = op->sz.n_owned;
+  HB_TRY(phase_event(op, op->t_p, true, st));
   hbk::cg_update_p<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
       op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n, lam_init(op), op->partials.as<double>(),
       op->scal.as<hbk::CgScalars>());
   op->launches++;
   CU_TRY(cudaGetLastError());
+  HB_TRY(phase_event(op, op->t_p, false, st));
+  op->last_timed = false;
   return HB_OK;
 }
 
@@ -669,14 +739,20 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
   HB_TRY(ensure_hist(op, K));
   hb_op::GraphKey key{K, b, x, op->profiling, st};
   auto it = op->graphs.find(key);
-  if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; }  // a profiling graph records into events 0..n-1
+  if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }  // a profiling graph records into events 0..n-1
   if (it == op->graphs.end()) {
     int64_t l0 = op->launches;
     cudaGraph_t graph;
     cudaStream_t cs = op->cap_stream;
     CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int status = cg_init(op, b, x, cs);
-    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
+    // with an L2 window the iterate lives in the arena (xs) and is copied out once at the end
+    double* xw = op->l2_window ? op->xs.as<double>() : x;
+    int status = cg_init(op, b, xw, cs);
+    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, xw, cs);
+    if (status == HB_OK && xw != x && op->sz.n_owned > 0) {
+      cudaError_t me = cudaMemcpyAsync(x, xw, (size_t)op->sz.n_owned * 8, cudaMemcpyDeviceToDevice, cs);
+      if (me != cudaSuccess) { set_error(std::string("cg_fixed: copy-out: ") + cudaGetErrorString(me)); status = HB_ERR_CUDA; }
+    }
     cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
     CU_TRY(ce);
@@ -684,10 +760,12 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
     cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     CU_TRY(ie);
-    it = op->graphs.emplace(key, hb_op::GraphVal{exec, op->launches - l0, op->prof_used}).first;
+    it = op->graphs.emplace(key, hb_op::GraphVal{exec, op->launches - l0, op->prof_used, op->t_xr.used, op->t_p.used}).first;
     op->launches = l0;
   }
   op->prof_used = it->second.prof_events;
+  op->t_xr.used = it->second.prof_xr;
+  op->t_p.used = it->second.prof_p;
   CU_TRY(cudaGraphLaunch(it->second.exec, st));
   op->launches += it->second.launches;
   return finish_result(op, K, rr_hist_host, res, st);
@@ -745,6 +823,17 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
   return HB_OK;
 }
 
+extern "C" int hb_l2_reset(void) {
+  CU_TRY(cudaCtxResetPersistingL2Cache());
+  return HB_OK;
+}
+
+extern "C" int hb_op_l2_resident_bytes(const hb_op* op, int64_t* bytes) {
+  if (!op || !bytes) { set_error("hb_op_l2_resident_bytes: null pointer"); return HB_ERR_ARG; }
+  *bytes = (int64_t)op->l2_window;
+  return HB_OK;
+}
+
 extern "C" int hb_op_set_profiling(hb_op* op, int enable) {
   if (!op || enable < 0) { set_error("hb_op_set_profiling: bad argument"); return HB_ERR_ARG; }
   const bool on = enable != 0;
@@ -757,6 +846,8 @@ extern "C" int hb_op_set_profiling(hb_op* op, int enable) {
   op->prof_stride = on ? enable : 1;
   op->prof_seq = 0;
   op->prof_used = 0;
+  op->t_xr.used = 0;
+  op->t_p.used = 0;
   return HB_OK;
 }
 
@@ -771,6 +862,24 @@ extern "C" int hb_op_kernel_time(hb_op* op, int64_t* launches, double* mean_seco
   }
   *launches = (int64_t)op->prof_used;
   *mean_seconds = op->prof_used ? tot / op->prof_used : 0.0;
+  return HB_OK;
+}
+
+extern "C" int hb_op_phase_times(hb_op* op, double* mean_seconds3) {
+  if (!op || !mean_seconds3) { set_error("hb_op_phase_times: null pointer"); return HB_ERR_ARG; }
+  int64_t n = 0;
+  HB_TRY(hb_op_kernel_time(op, &n, &mean_seconds3[0]));
+  hb_op::Timer* tms[2] = {&op->t_xr, &op->t_p};
+  for (int k = 0; k < 2; ++k) {
+    double tot = 0.0;
+    for (size_t t = 0; t < tms[k]->used; ++t) {
+      float ms = 0.f;
+      CU_TRY(cudaEventSynchronize(tms[k]->ev[t].second));
+      CU_TRY(cudaEventElapsedTime(&ms, tms[k]->ev[t].first, tms[k]->ev[t].second));
+      tot += ms * 1e-3;
+    }
+    mean_seconds3[1 + k] = tms[k]->used ? tot / tms[k]->used : 0.0;
+  }
   return HB_OK;
 }
 

@@ -15,7 +15,7 @@
 
 namespace hbk {
 
-constexpr int VEC_BLOCK = 256;
+constexpr int VEC_BLOCK = 512;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
