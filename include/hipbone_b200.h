@@ -163,13 +163,6 @@ int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t ma
  * of the last solve (or since enabling, outside graphs) and their mean duration in seconds. */
 int hb_op_set_profiling(hb_op* op, int enable);
 int hb_op_kernel_time(hb_op* op, int64_t* launches, double* mean_seconds);
-/* L2 residency.  When the index array and the CG vectors fit the device's persisting-L2
- * budget, hb_op_create marks them L2-persisting for the fixed-iteration CG graph (they are
- * re-read every iteration; the geometric factors stream from HBM).  hb_op_l2_resident_bytes
- * reports the window (0 = none; env HB_L2_PERSIST=0 disables).  hb_l2_reset returns all
- * persisting lines of the context to normal (call between timed steps for a cold start). */
-int hb_op_l2_resident_bytes(const hb_op* op, int64_t* bytes);
-int hb_l2_reset(void);
 /* Mean durations (seconds) of the timed CG phases of the last solve: [0] operator,
  * [1] x/r update (with the p.Ap reduction), [2] p update; 0 for a phase never timed (P > 1
  * vector phases are not timed). */

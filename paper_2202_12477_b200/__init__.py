@@ -5,5 +5,5 @@ Python surface = a thin ctypes binding (``hipbone.py``); every step of the path 
 library's sm_100a kernels.  The package never imports ``oracle/``.
 """
 from .hipbone import (Comm, Group, HBError, Mesh, Operator, comm_unique_id, gll, rank_grid,  # noqa: F401
-                      stream_bench, version, l2_reset, EXPORTED, LIB_PATH)
+                      stream_bench, version, EXPORTED, LIB_PATH)
 from . import ledger  # noqa: F401

@@ -70,7 +70,8 @@ struct LinesShape {
   static constexpr int MINB_REG0 = 65536 / (BLOCK * REGS);
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
-  static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
+  // N >= 12: one 256-thread CTA per SM without a register cap measured best (no spills)
+  static constexpr int MINB = N >= 12 ? 1 : (MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM));
 };
 
 // sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs
@@ -189,7 +190,14 @@ __device__ __forceinline__ void energy_finish(double en, const AxArgs& a, double
   }
 }
 
-template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0, bool PFL = true>
+template <bool CS>
+__device__ __forceinline__ double ldG(const double* p) {
+  if constexpr (CS) return __ldcs(p);
+  else return __ldg(p);
+}
+
+template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0, bool PFL = true,
+          bool GCS = true>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
@@ -290,8 +298,10 @@ ax_lines(const AxArgs a) {
         double grr = 0, grs = 0, grt = 0, gss = 0, gst = 0, gtt = 0;
         if (act) {
           const double* g = Ge + k * 6 * NP2;
-          grr = __ldg(g); grs = __ldg(g + NP2); grt = __ldg(g + 2 * NP2);
-          gss = __ldg(g + 3 * NP2); gst = __ldg(g + 4 * NP2); gtt = __ldg(g + 5 * NP2);
+          // G is read exactly once per apply: streaming (evict-first) loads keep it from
+          // displacing the gathered x / accumulated Ap lines that neighbouring elements reuse
+          grr = ldG<GCS>(g); grs = ldG<GCS>(g + NP2); grt = ldG<GCS>(g + 2 * NP2);
+          gss = ldG<GCS>(g + 3 * NP2); gst = ldG<GCS>(g + 4 * NP2); gtt = ldG<GCS>(g + 5 * NP2);
         }
         const int o = S::at(ca, cb, k);
         const double ur = s_r[o], us = s_s[o], ut = gt[0][k];

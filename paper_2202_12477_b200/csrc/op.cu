@@ -90,10 +90,11 @@ struct AxKernel {
   size_t smem = 0;
 };
 
-template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0, bool PFL = true>
+template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0, bool PFL = true,
+          bool GCS = true>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
@@ -109,18 +110,28 @@ AxKernel pick_ax_n(bool halo, bool massb) {
 }
 
 // experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
-AxKernel pick_ax_variant(int v) {
+AxKernel pick_ax_variant(int N, int v) {
+  if (N == 15) {
+    switch (v) {
+      case 1: return make_lines<15, false, false, 0, 1>();                      // no register cap
+      case 2: return make_lines<15, false, false, 0, 2, 0, false>();            // no G prefetch
+      case 3: return make_lines<15, false, false, 0, 2, 0, true, false>();      // G cached normally
+      case 4: return make_lines<15, false, false, 0, 1, 0, false>();            // no cap, no prefetch
+      default: return make_lines<15, false, false, kLinesPF>();
+    }
+  }
   switch (v) {
-    case 1: return make_lines<7, false, false, 0, 10, 1>();         // 96 regs
-    case 2: return make_lines<7, false, false, 0, 8, 1, false>();   // no L2 prefetch of G
+    case 1: return make_lines<7, false, false, 0, 8, 0, true, false>();   // G cached normally
+    case 2: return make_lines<7, false, false, 0, 8, 0, false>();         // no L2 prefetch of G
     default: return make_lines<7, false, false, kLinesPF>();
   }
 }
 
 AxKernel pick_ax(int N, bool halo, bool massb) {
-  if (N == 7 && !halo && !massb) {
+  if ((N == 7 || N == 15) && !halo && !massb) {
     const char* v = getenv("HB_AX_VARIANT");
-    if (v && atoi(v) > 0) return pick_ax_variant(atoi(v));
+    const char* vn = getenv("HB_AX_VN");
+    if (v && atoi(v) > 0 && (vn ? atoi(vn) : 7) == N) return pick_ax_variant(N, atoi(v));
   }
   switch (N) {
     case 1: return pick_ax_n<1>(halo, massb);
@@ -197,8 +208,7 @@ struct hb_op {
   bool grouped = false;
   int64_t nA = 0, nH = 0, nB = 0;
   // device data
-  DevBuf arena;  // [idx | r | p | Ap | xs]: the data re-read every CG iteration, one L2 window
-  size_t l2_window = 0;  // bytes of the arena marked L2-persisting for the captured CG graph
+  DevBuf arena;  // [idx | r | p | Ap | xs]: the data every CG iteration re-reads besides G
   DevBuf idx, G, B, owned_gid;
   DevBuf r, p, Ap, xs, partials, e_part, scal, hist, dot_out, dot_ticket;
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
@@ -552,30 +562,6 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     CU_TRY(cudaStreamCreateWithPriority(&op->comm_stream, cudaStreamNonBlocking, hi));
   }
   CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
-  // L2 residency (B200: 126 MB L2): when the arena fits the persisting-L2 budget, kernels
-  // captured from cap_stream (the fixed-iteration CG graph) keep idx and the CG vectors
-  // L2-resident across iterations while G streams from HBM.  HB_L2_PERSIST=0 disables.
-  {
-    const char* env = getenv("HB_L2_PERSIST");
-    int dev = 0, maxp = 0, maxw = 0;
-    CU_TRY(cudaGetDevice(&dev));
-    CU_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
-    CU_TRY(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-    const size_t want = op->arena.bytes;
-    if (!(env && env[0] == '0') && want > 0 && want <= (size_t)maxp && want <= (size_t)maxw) {
-      size_t cur = 0;
-      CU_TRY(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-      if (cur < want) CU_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-      cudaStreamAttrValue v = {};
-      v.accessPolicyWindow.base_ptr = op->arena.p;
-      v.accessPolicyWindow.num_bytes = want;
-      v.accessPolicyWindow.hitRatio = 1.0f;
-      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      CU_TRY(cudaStreamSetAttribute(op->cap_stream, cudaStreamAttributeAccessPolicyWindow, &v));
-      op->l2_window = want;
-    }
-  }
   for (cudaEvent_t* e : {&op->ev_pack, &op->ev_halo, &op->ev_haloel, &op->ev_gather, &op->ev_red, &op->ev_red_done, &op->ev_cap})
     CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CU_TRY(cudaStreamSynchronize(st));
@@ -745,14 +731,8 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
     cudaGraph_t graph;
     cudaStream_t cs = op->cap_stream;
     CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    // with an L2 window the iterate lives in the arena (xs) and is copied out once at the end
-    double* xw = op->l2_window ? op->xs.as<double>() : x;
-    int status = cg_init(op, b, xw, cs);
-    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, xw, cs);
-    if (status == HB_OK && xw != x && op->sz.n_owned > 0) {
-      cudaError_t me = cudaMemcpyAsync(x, xw, (size_t)op->sz.n_owned * 8, cudaMemcpyDeviceToDevice, cs);
-      if (me != cudaSuccess) { set_error(std::string("cg_fixed: copy-out: ") + cudaGetErrorString(me)); status = HB_ERR_CUDA; }
-    }
+    int status = cg_init(op, b, x, cs);
+    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
     cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
     CU_TRY(ce);
@@ -820,17 +800,6 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
   HB_TRY(hb_cg_solve(op, b_dev, op->xs.as<double>(), max_iters, eps, rr_hist_host, res, stream));
   if (bytes) CU_TRY(cudaMemcpyAsync(x_host, op->xs.p, bytes, cudaMemcpyDeviceToHost, st));
   CU_TRY(cudaStreamSynchronize(st));
-  return HB_OK;
-}
-
-extern "C" int hb_l2_reset(void) {
-  CU_TRY(cudaCtxResetPersistingL2Cache());
-  return HB_OK;
-}
-
-extern "C" int hb_op_l2_resident_bytes(const hb_op* op, int64_t* bytes) {
-  if (!op || !bytes) { set_error("hb_op_l2_resident_bytes: null pointer"); return HB_ERR_ARG; }
-  *bytes = (int64_t)op->l2_window;
   return HB_OK;
 }
 

@@ -86,9 +86,7 @@ _SIGS = {
     "hb_op_set_profiling": (C.c_int, [_p, C.c_int]),
     "hb_op_kernel_time": (C.c_int, [_p, _i64p, _dp]),
     "hb_op_launch_count": (C.c_int, [_p, _i64p]),
-    "hb_op_l2_resident_bytes": (C.c_int, [_p, _i64p]),
     "hb_op_phase_times": (C.c_int, [_p, _dp]),
-    "hb_l2_reset": (C.c_int, []),
     "hb_op_sizes": (C.c_int, [_p, C.POINTER(hb_sizes)]),
     "hb_op_destroy": (C.c_int, [_p]),
     "hb_group_create": (C.c_int, [C.POINTER(_p), C.c_int, C.POINTER(_p)]),
@@ -148,11 +146,6 @@ def rank_grid(P: int, nx: int, ny: int, nz: int):
     g = np.zeros(3, dtype=np.int32)
     _check(_lib.hb_rank_grid(P, nx, ny, nz, _ptr(g, C.c_int32)))
     return tuple(int(v) for v in g)
-
-
-def l2_reset():
-    """Return all L2-persisting lines to normal (cold start between timed steps)."""
-    _check(_lib.hb_l2_reset())
 
 
 def stream_bench(n_out: int, reps: int = 20) -> float:
@@ -321,11 +314,6 @@ class Operator:
         a = np.zeros(3)
         _check(_lib.hb_op_phase_times(self._h, _ptr(a, C.c_double)))
         return tuple(float(v) for v in a)
-
-    def l2_resident_bytes(self) -> int:
-        n = C.c_int64()
-        _check(_lib.hb_op_l2_resident_bytes(self._h, C.byref(n)))
-        return n.value
 
     def launch_count(self) -> int:
         n = C.c_int64()
