@@ -210,7 +210,8 @@ struct hb_op {
   // device data
   DevBuf arena;  // [idx | r | p | Ap | xs]: the data every CG iteration re-reads besides G
   DevBuf idx, G, B, owned_gid;
-  DevBuf r, p, Ap, xs, partials, e_part, scal, hist, dot_out, dot_ticket;
+  DevBuf r, p, Ap, xs, partials, e_part, pp_part, scal, hist, dot_out, dot_ticket;
+  int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
   std::vector<int32_t> nbr;
   std::vector<int64_t> soff, scnt, roff, rcnt;
@@ -556,6 +557,17 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     k->grid_max = std::max(1, nb) * num_sms();
   }
   HB_TRY(op->e_part.alloc((size_t)std::max(op->ax_plain.grid_max, op->ax_halo.grid_max) * 8 + 64));
+  // P = 1: fused cooperative vector update (grid barrier instead of a second kernel)
+  if (m->P == 1 && !comm) {
+    int dev = 0, coop = 0, nb = 0;
+    CU_TRY(cudaGetDevice(&dev));
+    CU_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)&hbk::cg_update_fused, hbk::VEC_BLOCK, 0));
+    const char* env = getenv("HB_FUSED_UPDATE");
+    if (coop && nb > 0 && !(env && env[0] == '0'))
+      op->fused_grid = std::min(vec_grid(std::max<int64_t>(n, 1)), nb * num_sms());
+  }
+  HB_TRY(op->pp_part.alloc((size_t)std::max(op->fused_grid, 1) * 8 + 64));
   if (m->P > 1 && comm) {
     int lo, hi;
     CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -635,9 +647,10 @@ double lam_pp(const hb_op* op) { return op->mass_mode == 0 ? op->lam : 0.0; }
 
 int cg_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
   const int64_t n = op->sz.n_owned;
-  hbk::cg_init<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+  const bool fused = op->fused_grid > 0;
+  hbk::cg_init<<<fused ? op->fused_grid : vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
       b, x, op->r.as<double>(), op->p.as<double>(), op->Ap.as<double>(), n, lam_init(op),
-      op->partials.as<double>(), op->scal.as<hbk::CgScalars>());
+      op->partials.as<double>(), op->scal.as<hbk::CgScalars>(), fused ? op->pp_part.as<double>() : nullptr);
   op->launches++;
   CU_TRY(cudaGetLastError());
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
@@ -650,6 +663,25 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
   const int gv = vec_grid(std::max<int64_t>(n, 1));
   HB_TRY(allreduce_sum(op, &s->pAp, st));
+  if (op->fused_grid > 0) {  // one GPU: the whole vector part of the iteration, one cooperative kernel
+    HB_TRY(phase_event(op, op->t_xr, true, st));
+    double* xp = x;
+    double* pp = op->p.as<double>();
+    double* rp = op->r.as<double>();
+    double* ap = op->Ap.as<double>();
+    int64_t nn = n;
+    const double* ep = op->e_part.as<double>();
+    int nep = op->last_grid;
+    double* ppp = op->pp_part.as<double>();
+    double lpp = lam_pp(op), li = lam_init(op);
+    double* rrp = op->partials.as<double>();
+    double* hp = op->hist.as<double>();
+    void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &ppp, &lpp, &li, &rrp, &s, &hp};
+    CU_TRY(cudaLaunchCooperativeKernel((const void*)&hbk::cg_update_fused, dim3(op->fused_grid),
+                                       dim3(hbk::VEC_BLOCK), args, 0, st));
+    op->launches++;
+    return phase_event(op, op->t_xr, false, st);
+  }
   if (!op->comm || op->comm->P == 1) {  // one GPU: energy reduction + x and r updates in one pass
     HB_TRY(phase_event(op, op->t_xr, true, st));
     hbk::cg_update_xr_e<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(),
@@ -677,6 +709,10 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
 
 int cg_vec_part2(hb_op* op, cudaStream_t st) {
   const int64_t n = op->sz.n_owned;
+  if (op->fused_grid > 0) {  // done inside cg_update_fused
+    op->last_timed = false;
+    return HB_OK;
+  }
   HB_TRY(phase_event(op, op->t_p, true, st));
   hbk::cg_update_p<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
       op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n, lam_init(op), op->partials.as<double>(),

@@ -11,6 +11,8 @@
 #pragma once
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"  // CgScalars
 
 namespace hbk {
@@ -67,12 +69,17 @@ __device__ __forceinline__ bool finish_reduction(double v, double* partials, uin
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_init(const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r,
         double* __restrict__ p, double* __restrict__ Ap, int64_t n, double lam_init,
-        double* partials, CgScalars* s) {
+        double* partials, CgScalars* s, double* pp_part) {
   double acc = 0.0;
   for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK) {
     double v = b[l];
     r[l] = v; p[l] = v; x[l] = 0.0; Ap[l] = lam_init * v;
     acc = fma(v, v, acc);
+  }
+  if (pp_part) {  // p = r: the CTA partials of p.p for the fused update's first p.Ap
+    const double bs = block_sum(acc);
+    if (threadIdx.x == 0) pp_part[blockIdx.x] = bs;
+    __syncthreads();
   }
   double tot;
   if (finish_reduction(acc, partials, &s->ticket, &tot)) {
@@ -156,6 +163,96 @@ cg_update_xr_e(double* __restrict__ x, const double* __restrict__ p, double* __r
     s->rr = rr;
     if (hist) hist[s->it] = rr;
     s->rr_new = tot;
+  }
+}
+
+// One GPU, whole vector update of an iteration in one cooperative kernel (grid barrier
+// instead of a kernel boundary): p.Ap = sum(e_part) + lambda sum(pp_part) (deterministic,
+// every CTA alike); x += alpha p, r -= alpha Ap, CTA partial of r.r; grid barrier; every CTA
+// sums the r.r partials in CTA order -> beta; p = r + beta p, Ap = lambda p, CTA partial of
+// p.p (consumed by the next iteration's p.Ap).  r and p are re-read after the barrier from L2
+// when the vectors fit it.  CTA 0 publishes the scalars (pAp, rr, rr_new, history, j).
+__global__ void __launch_bounds__(VEC_BLOCK)
+cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
+                int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
+                double lam_init, double* rr_part, CgScalars* s, double* hist) {
+  __shared__ double s_b[2];
+  // ---- p.Ap and alpha (identical in every CTA)
+  double ev = 0.0, pv_ = 0.0;
+  for (int b = threadIdx.x; b < n_epart; b += VEC_BLOCK) ev += e_part[b];
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) pv_ += pp_part[b];
+  ev = block_sum(ev);
+  __syncthreads();
+  pv_ = block_sum(pv_);
+  const double rr = s->rr_new;  // r_j.r_j
+  if (threadIdx.x == 0) s_b[0] = ev + lam_pp * pv_;
+  __syncthreads();
+  const double pAp = s_b[0];
+  const double alpha = (pAp != 0.0) ? rr / pAp : 0.0;  // c15 guard
+  // ---- x, r update + r.r
+  const int64_t n2 = n >> 1;
+  const int64_t stride = (int64_t)gridDim.x * VEC_BLOCK;
+  double acc = 0.0;
+  {
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* a2 = reinterpret_cast<const double2*>(Ap);
+    for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += stride) {
+      double2 xv = x2[l], pv = p2[l], rv = r2[l], av = a2[l];
+      xv.x = fma(alpha, pv.x, xv.x); xv.y = fma(alpha, pv.y, xv.y);
+      rv.x = fma(-alpha, av.x, rv.x); rv.y = fma(-alpha, av.y, rv.y);
+      x2[l] = xv; r2[l] = rv;
+      acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t l = n - 1;
+      x[l] = fma(alpha, p[l], x[l]);
+      const double rv = fma(-alpha, Ap[l], r[l]);
+      r[l] = rv;
+      acc = fma(rv, rv, acc);
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) rr_part[blockIdx.x] = acc;
+  cooperative_groups::this_grid().sync();
+  // ---- beta (identical in every CTA), p update + p.p
+  double rn = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) rn += __ldcg(rr_part + b);
+  rn = block_sum(rn);
+  if (threadIdx.x == 0) s_b[1] = rn;
+  __syncthreads();
+  const double rr_new = s_b[1];
+  const double beta = (rr != 0.0) ? rr_new / rr : 0.0;  // c15 guard
+  double acc2 = 0.0;
+  {
+    double2* p2 = reinterpret_cast<double2*>(p);
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    double2* a2 = reinterpret_cast<double2*>(Ap);
+    for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += stride) {
+      double2 pv = p2[l], rv = __ldcg(r2 + l);
+      pv.x = fma(beta, pv.x, rv.x); pv.y = fma(beta, pv.y, rv.y);
+      p2[l] = pv;
+      a2[l] = make_double2(lam_init * pv.x, lam_init * pv.y);
+      acc2 = fma(pv.x, pv.x, acc2); acc2 = fma(pv.y, pv.y, acc2);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t l = n - 1;
+      const double pv = fma(beta, p[l], __ldcg(r + l));
+      p[l] = pv; Ap[l] = lam_init * pv;
+      acc2 = fma(pv, pv, acc2);
+    }
+  }
+  acc2 = block_sum(acc2);
+  if (threadIdx.x == 0) {
+    pp_part[blockIdx.x] = acc2;  // every CTA read the old partials before the grid barrier
+    if (blockIdx.x == 0) {
+      s->pAp = pAp;
+      s->rr = rr;
+      if (hist) hist[s->it] = rr;
+      s->rr_new = rr_new;
+      s->it += 1;
+    }
   }
 }
 
