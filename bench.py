@@ -303,7 +303,7 @@ def main():
             traffic = pj.get("dram_bytes_per_launch", {}).get(key)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": f"ax_layered<N={N}>", "launch_ms": round(mean_s * 1e3, 4), "launches_timed": n_l,
+                "kernel": f"ax_lines<N={N}>", "launch_ms": round(mean_s * 1e3, 4), "launches_timed": n_l,
                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                 "paper_ledger_gbs": round(ledger.op_bytes_paper(n, NL_loc) / mean_s / 1e9, 1),
                 "op_gflops": round(ledger.op_flops(s["E_local"], N) / mean_s / 1e9, 1)}
@@ -312,11 +312,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(box, N, args.cpu_seconds)
 
+    wname = {((16, 16, 16), 7): "C2", ((52, 52, 52), 7): "C3 N=7", ((66, 66, 66), 7): "C4 (1 GPU)",
+             ((50, 50, 48), 15): "C5 (1 GPU)"}.get((tuple(blk), N), "custom")
     if rank == 0:
         out = {"metric": METRIC, "value": round(fom, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": f"C2: N={N}, E={box[0]}x{box[1]}x{box[2]} box, {K} CG iterations per step"
+               "config": {"workload": f"{wname}: N={N}, E={box[0]}x{box[1]}x{box[2]} box, {K} CG iterations per step"
                                       + (f" (C4-shaped weak scaling, {blk[0]}x{blk[1]}x{blk[2]} per GPU)" if world > 1 else ""),
                           "box": list(box), "N": N, "E": E_glob, "N_G": NG, "N_L": E_glob * (N + 1) ** 3,
                           "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
