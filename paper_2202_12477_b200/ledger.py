@@ -42,9 +42,10 @@ def cg_bytes_paper(NG: int, NL: int) -> int:
 
 
 def cg_bytes_fused(NG: int, NL: int, mass_mode: int = 0) -> int:
-    """This build per CG iteration: operator (24 N_G + 52 N_L) + p.Ap (16 N_G) +
-    x,r update with r.r (48 N_G) + p update writing lambda p (32 N_G)."""
-    return op_bytes_fused(NG, NL, mass_mode) + 96 * NG
+    """This build per CG iteration: operator (24 N_G + 52 N_L, p.Ap fused in as the element
+    energy) + the vector update (x, p, r, Ap read; x, r, p, Ap written: 64 N_G; the
+    r.r-dependent p update re-reads r and p, counted once more: 80 N_G)."""
+    return op_bytes_fused(NG, NL, mass_mode) + 80 * NG
 
 
 def op_roofline(N: int, B: float, C: float = float("inf")) -> float:
