@@ -364,24 +364,66 @@ int stage_unpack(hb_op* op, double* y, cudaStream_t st) {
   return HB_OK;
 }
 
-int nccl_halo_exchange(hb_op* op, cudaStream_t cs) {
-  NC_TRY(ncclGroupStart());
+// Point-to-point messages of the two exchanges of one apply.  The halo segment of
+// the extended vector is the receive buffer of the halo exchange and the send buffer of the
+// assembly exchange (zero copy).  Both transports (NCCL, loopback) consume these lists.
+struct Msg {
+  double* buf;
+  int64_t count;
+  int peer;
+};
+void halo_msgs(hb_op* op, std::vector<Msg>& sends, std::vector<Msg>& recvs) {
+  sends.clear(); recvs.clear();
   for (size_t q = 0; q < op->nbr.size(); ++q) {
-    if (op->scnt[q]) NC_TRY(ncclSend(op->send_buf.as<double>() + op->soff[q], op->scnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
-    if (op->rcnt[q]) NC_TRY(ncclRecv(op->xh.as<double>() + op->roff[q], op->rcnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
+    if (op->scnt[q]) sends.push_back({op->send_buf.as<double>() + op->soff[q], op->scnt[q], op->nbr[q]});
+    if (op->rcnt[q]) recvs.push_back({op->xh.as<double>() + op->roff[q], op->rcnt[q], op->nbr[q]});
   }
+}
+void assembly_msgs(hb_op* op, std::vector<Msg>& sends, std::vector<Msg>& recvs) {
+  sends.clear(); recvs.clear();
+  for (size_t q = 0; q < op->nbr.size(); ++q) {
+    if (op->rcnt[q]) sends.push_back({op->yh.as<double>() + op->roff[q], op->rcnt[q], op->nbr[q]});
+    if (op->scnt[q]) recvs.push_back({op->recv_buf.as<double>() + op->soff[q], op->scnt[q], op->nbr[q]});
+  }
+}
+
+int nccl_exchange(hb_op* op, const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t cs) {
+  NC_TRY(ncclGroupStart());
+  for (const Msg& m : sends) NC_TRY(ncclSend(m.buf, m.count, ncclFloat64, m.peer, op->comm->nccl, cs));
+  for (const Msg& m : recvs) NC_TRY(ncclRecv(m.buf, m.count, ncclFloat64, m.peer, op->comm->nccl, cs));
   NC_TRY(ncclGroupEnd());
   return HB_OK;
 }
 
-int nccl_assembly_exchange(hb_op* op, cudaStream_t cs) {
-  NC_TRY(ncclGroupStart());
-  for (size_t q = 0; q < op->nbr.size(); ++q) {
-    if (op->rcnt[q]) NC_TRY(ncclSend(op->yh.as<double>() + op->roff[q], op->rcnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
-    if (op->scnt[q]) NC_TRY(ncclRecv(op->recv_buf.as<double>() + op->soff[q], op->scnt[q], ncclFloat64, op->nbr[q], op->comm->nccl, cs));
-  }
-  NC_TRY(ncclGroupEnd());
+// Per-rank phases of the split apply, shared by the NCCL path and loopback groups.
+// `exchange(kind, cs)` moves the messages of the halo (kind 0) or assembly (kind 1) exchange
+// on the communication stream cs; ev_pack / ev_haloel mark when this rank's send data is ready.
+template <class Exchange>
+int rank_phase_halo(hb_op* op, const double* x, double* y, cudaStream_t st, cudaStream_t cs, bool energy, int last,
+                    Exchange&& exchange) {
+  HB_TRY(exchange(0, cs));
+  CU_TRY(cudaEventRecord(op->ev_halo, cs));
+  HB_TRY(launch_ax(op, op->ax_plain, 0, op->nA, x, y, st, energy, last == 0));                  // interior A
+  CU_TRY(cudaStreamWaitEvent(st, op->ev_halo, 0));
+  HB_TRY(launch_ax(op, op->ax_halo, op->nA, op->nA + op->nH, x, y, st, energy, last == 1));     // halo elements
+  CU_TRY(cudaEventRecord(op->ev_haloel, st));
   return HB_OK;
+}
+
+template <class Exchange>
+int rank_phase_assembly(hb_op* op, const double* x, double* y, cudaStream_t st, cudaStream_t cs, bool energy,
+                        int last, Exchange&& exchange) {
+  CU_TRY(cudaStreamWaitEvent(cs, op->ev_haloel, 0));
+  HB_TRY(exchange(1, cs));
+  CU_TRY(cudaEventRecord(op->ev_gather, cs));
+  HB_TRY(launch_ax(op, op->ax_plain, op->nA + op->nH, op->sz.E_local, x, y, st, energy, last == 2));  // interior B
+  CU_TRY(cudaStreamWaitEvent(st, op->ev_gather, 0));
+  return stage_unpack(op, y, st);
+}
+
+int last_launch(const hb_op* op) {  // the last non-empty launch publishes p.Ap
+  const int64_t nB = op->sz.E_local - op->nA - op->nH;
+  return nB > 0 ? 2 : (op->nH > 0 ? 1 : 0);
 }
 
 // y = A x for one op (P = 1, or P > 1 with NCCL).  init_y=false: y already holds the
@@ -394,25 +436,18 @@ int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStrea
     HB_TRY(stage_init(op, x, y, init_y, st));
     return launch_ax(op, op->ax_plain, 0, E, x, y, st, energy, true);
   }
-  // the last non-empty launch publishes p.Ap
-  const int64_t nA = op->nA, nH = op->nH, nB = E - nA - nH;
-  const int last = nB > 0 ? 2 : (nH > 0 ? 1 : 0);
+  const int last = last_launch(op);
   cudaStream_t cs = op->comm_stream;
+  auto nccl = [op](int kind, cudaStream_t c) -> int {
+    std::vector<Msg> snd, rcv;
+    if (kind == 0) halo_msgs(op, snd, rcv); else assembly_msgs(op, snd, rcv);
+    return nccl_exchange(op, snd, rcv, c);
+  };
   HB_TRY(stage_init(op, x, y, init_y, st));
   CU_TRY(cudaEventRecord(op->ev_pack, st));
   CU_TRY(cudaStreamWaitEvent(cs, op->ev_pack, 0));
-  HB_TRY(nccl_halo_exchange(op, cs));
-  CU_TRY(cudaEventRecord(op->ev_halo, cs));
-  HB_TRY(launch_ax(op, op->ax_plain, 0, nA, x, y, st, energy, last == 0));                      // interior A
-  CU_TRY(cudaStreamWaitEvent(st, op->ev_halo, 0));
-  HB_TRY(launch_ax(op, op->ax_halo, nA, nA + nH, x, y, st, energy, last == 1));                 // halo elements
-  CU_TRY(cudaEventRecord(op->ev_haloel, st));
-  CU_TRY(cudaStreamWaitEvent(cs, op->ev_haloel, 0));
-  HB_TRY(nccl_assembly_exchange(op, cs));
-  CU_TRY(cudaEventRecord(op->ev_gather, cs));
-  HB_TRY(launch_ax(op, op->ax_plain, nA + nH, E, x, y, st, energy, last == 2));                 // interior B
-  CU_TRY(cudaStreamWaitEvent(st, op->ev_gather, 0));
-  return stage_unpack(op, y, st);
+  HB_TRY(rank_phase_halo(op, x, y, st, cs, energy, last, nccl));
+  return rank_phase_assembly(op, x, y, st, cs, energy, last, nccl);
 }
 
 }  // namespace
@@ -909,8 +944,16 @@ extern "C" int hb_op_destroy(hb_op* op) {
 // ------------------------------------------------------------------ loopback groups
 struct hb_group {
   std::vector<hb_op*> ops;
-  std::vector<std::vector<int>> peer_index;  // [rank][q] -> index of `rank` in nbr list of nbr[q]
-  DevBuf sums;                               // per-rank scalar staging
+  std::vector<cudaStream_t> st, cs;  // per virtual rank: compute and communication streams
+  std::vector<cudaEvent_t> done;     // per virtual rank: end of its apply
+  cudaEvent_t start = nullptr;
+  DevBuf sums;                       // pointer table of the allreduce stand-in
+  ~hb_group() {
+    for (cudaStream_t x : st) cudaStreamDestroy(x);
+    for (cudaStream_t x : cs) cudaStreamDestroy(x);
+    for (cudaEvent_t e : done) cudaEventDestroy(e);
+    if (start) cudaEventDestroy(start);
+  }
 };
 
 extern "C" int hb_group_create(hb_op* const* ops, int P, hb_group** out) {
@@ -925,20 +968,32 @@ extern "C" int hb_group_create(hb_op* const* ops, int P, hb_group** out) {
     }
     g->ops.push_back(ops[r]);
   }
-  g->peer_index.resize(P);
+  // plan consistency: what r sends to q is what q expects from r
   for (int r = 0; r < P; ++r) {
     hb_op* a = g->ops[r];
     for (size_t q = 0; q < a->nbr.size(); ++q) {
       hb_op* b = g->ops[a->nbr[q]];
       auto itq = std::find(b->nbr.begin(), b->nbr.end(), r);
       if (itq == b->nbr.end()) { set_error("hb_group_create: asymmetric neighbour sets"); delete g; return HB_ERR_SETUP; }
-      int back = (int)(itq - b->nbr.begin());
+      const size_t back = (size_t)(itq - b->nbr.begin());
       if (a->scnt[q] != b->rcnt[back] || a->rcnt[q] != b->scnt[back]) {
         set_error("hb_group_create: send/recv plan sizes disagree"); delete g; return HB_ERR_SETUP;
       }
-      g->peer_index[r].push_back(back);
     }
-    a->grouped = true;
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  g->st.resize(P); g->cs.resize(P); g->done.resize(P);
+  for (int r = 0; r < P; ++r) {
+    if (cudaStreamCreateWithFlags(&g->st[r], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&g->cs[r], cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming) != cudaSuccess) {
+      set_error("hb_group_create: stream/event creation failed"); delete g; return HB_ERR_CUDA;
+    }
+    g->ops[r]->grouped = true;
+  }
+  if (cudaEventCreateWithFlags(&g->start, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("hb_group_create: event creation failed"); delete g; return HB_ERR_CUDA;
   }
   int st = g->sums.alloc(8 * P);
   if (st) { delete g; return st; }
@@ -947,58 +1002,47 @@ extern "C" int hb_group_create(hb_op* const* ops, int P, hb_group** out) {
 }
 
 namespace {
-// device-to-device "transport": what rank r sends to nbr[q] lands in that rank's buffer
-int group_halo_exchange(hb_group* g, cudaStream_t st) {
-  for (size_t r = 0; r < g->ops.size(); ++r) {
-    hb_op* a = g->ops[r];
-    for (size_t q = 0; q < a->nbr.size(); ++q) {
-      hb_op* b = g->ops[a->nbr[q]];
-      int back = g->peer_index[r][q];
-      if (a->scnt[q])
-        CU_TRY(cudaMemcpyAsync(b->xh.as<double>() + b->roff[back], a->send_buf.as<double>() + a->soff[q],
-                               a->scnt[q] * 8, cudaMemcpyDeviceToDevice, st));
-    }
+// Loopback transport: rank r pulls each message addressed to it from the sender's buffer on
+// r's communication stream, after the sender's data-ready event (ev_pack for the halo
+// exchange, ev_haloel for the assembly exchange) -- the same message lists NCCL gets.
+int loopback_exchange(hb_group* g, int r, int kind, cudaStream_t cs) {
+  hb_op* a = g->ops[r];
+  std::vector<Msg> snd, rcv, psnd, prcv;
+  if (kind == 0) halo_msgs(a, snd, rcv); else assembly_msgs(a, snd, rcv);
+  for (const Msg& m : rcv) {
+    hb_op* b = g->ops[m.peer];
+    if (kind == 0) halo_msgs(b, psnd, prcv); else assembly_msgs(b, psnd, prcv);
+    const Msg* match = nullptr;
+    for (const Msg& ps : psnd) if (ps.peer == r) match = &ps;
+    if (!match || match->count != m.count) { set_error("loopback_exchange: unmatched message"); return HB_ERR_SETUP; }
+    CU_TRY(cudaStreamWaitEvent(cs, kind == 0 ? b->ev_pack : b->ev_haloel, 0));
+    CU_TRY(cudaMemcpyAsync(m.buf, match->buf, (size_t)m.count * 8, cudaMemcpyDeviceToDevice, cs));
   }
   return HB_OK;
 }
 
-int group_assembly_exchange(hb_group* g, cudaStream_t st) {
-  for (size_t r = 0; r < g->ops.size(); ++r) {
-    hb_op* a = g->ops[r];
-    for (size_t q = 0; q < a->nbr.size(); ++q) {
-      hb_op* b = g->ops[a->nbr[q]];
-      int back = g->peer_index[r][q];
-      if (a->rcnt[q])
-        CU_TRY(cudaMemcpyAsync(b->recv_buf.as<double>() + b->soff[back], a->yh.as<double>() + a->roff[q],
-                               a->rcnt[q] * 8, cudaMemcpyDeviceToDevice, st));
-    }
-  }
-  return HB_OK;
-}
-
+// The split apply of all virtual ranks, each on its own compute + communication stream with
+// the NCCL path's events: packs first (so every data-ready event exists before anyone waits
+// on it), then every rank's halo phase, then every rank's assembly phase.
 int group_apply_internal(hb_group* g, const double* const* x, double* const* y, bool init_y, cudaStream_t st,
                          bool energy = false) {
-  const size_t P = g->ops.size();
-  auto last_of = [](hb_op* a) {
-    const int64_t nB = a->sz.E_local - a->nA - a->nH;
-    return nB > 0 ? 2 : (a->nH > 0 ? 1 : 0);
-  };
-  for (size_t r = 0; r < P; ++r) HB_TRY(stage_init(g->ops[r], x[r], y[r], init_y, st));
-  HB_TRY(group_halo_exchange(g, st));
-  for (size_t r = 0; r < P; ++r) {
-    hb_op* a = g->ops[r];
-    HB_TRY(launch_ax(a, a->ax_plain, 0, a->nA, x[r], y[r], st, energy, last_of(a) == 0));
+  const int P = (int)g->ops.size();
+  CU_TRY(cudaEventRecord(g->start, st));
+  for (int r = 0; r < P; ++r) {
+    CU_TRY(cudaStreamWaitEvent(g->st[r], g->start, 0));
+    HB_TRY(stage_init(g->ops[r], x[r], y[r], init_y, g->st[r]));
+    CU_TRY(cudaEventRecord(g->ops[r]->ev_pack, g->st[r]));
   }
-  for (size_t r = 0; r < P; ++r) {
-    hb_op* a = g->ops[r];
-    HB_TRY(launch_ax(a, a->ax_halo, a->nA, a->nA + a->nH, x[r], y[r], st, energy, last_of(a) == 1));
+  for (int r = 0; r < P; ++r) {
+    auto ex = [g, r](int kind, cudaStream_t c) { return loopback_exchange(g, r, kind, c); };
+    HB_TRY(rank_phase_halo(g->ops[r], x[r], y[r], g->st[r], g->cs[r], energy, last_launch(g->ops[r]), ex));
   }
-  HB_TRY(group_assembly_exchange(g, st));
-  for (size_t r = 0; r < P; ++r) {
-    hb_op* a = g->ops[r];
-    HB_TRY(launch_ax(a, a->ax_plain, a->nA + a->nH, a->sz.E_local, x[r], y[r], st, energy, last_of(a) == 2));
+  for (int r = 0; r < P; ++r) {
+    auto ex = [g, r](int kind, cudaStream_t c) { return loopback_exchange(g, r, kind, c); };
+    HB_TRY(rank_phase_assembly(g->ops[r], x[r], y[r], g->st[r], g->cs[r], energy, last_launch(g->ops[r]), ex));
+    CU_TRY(cudaEventRecord(g->done[r], g->st[r]));
   }
-  for (size_t r = 0; r < P; ++r) HB_TRY(stage_unpack(g->ops[r], y[r], st));
+  for (int r = 0; r < P; ++r) CU_TRY(cudaStreamWaitEvent(st, g->done[r], 0));
   return HB_OK;
 }
 

@@ -1,0 +1,84 @@
+#!/usr/bin/env python
+"""Multi-rank NCCL path self-test: P processes (torchrun), each with its own hb_comm, run the
+split operator (halo exchange || interior A, halo elements, assembly exchange || interior B)
+and CG, then rank 0 compares the assembled result with the CPU oracle.
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 scripts/nccl_selftest.py
+Ranks use GPU (LOCAL_RANK % device_count) -- with one GPU several ranks share it, if NCCL allows.
+Prints one JSON line on rank 0."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    lr = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(lr % torch.cuda.device_count())
+    dist.init_process_group("gloo")
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    dist.barrier()
+    import paper_2202_12477_b200 as hb
+    box, N = (4, 3, 4), 3
+    uid = [hb.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    out = {"P": P, "ok": False}
+    try:
+        comm = hb.Comm(P, rank, uid[0])
+        m = hb.Mesh(*box, N, P=P, rank=rank)
+        op = hb.Operator(m, comm=comm)
+        n = op.n_owned
+        b = torch.empty(n, dtype=torch.float64, device="cuda")
+        op.forcing(2, b)
+        y = torch.empty_like(b)
+        op.apply(b, y)
+        bb = op.dot(b, b)
+        x = torch.zeros_like(b)
+        op.forcing(1, b)
+        K = 20
+        j, hist = op.cg(b, x, K)
+        torch.cuda.synchronize()
+        gathered = [None] * P
+        dist.all_gather_object(gathered, (m.owned(), y.cpu().numpy(), x.cpu().numpy()))
+        if rank == 0:
+            from oracle import basis, cg as ocg, forcing as of, mesh as om, operator as oo
+            xg, w, D = basis.basis(N)
+            E, NG, NL = om.global_sizes(*box, N)
+            gid = om.l2g(*box, N)
+            G = om.geometric_factors(E, N, w)
+            W = om.weights_W(gid, NG)
+            A = lambda v: oo.apply(v, gid, D, G, 1.0, W)
+            b2 = of.forcing(range(NG), 2)
+            yo = A(b2)
+            s = oo.apply_abs(b2, gid, D, G, 1.0, W)
+            yg = np.zeros(NG)
+            xgv = np.zeros(NG)
+            for own, yy, xx in gathered:
+                yg[own] = yy
+                xgv[own] = xx
+            b1 = of.forcing(range(NG), 1)
+            xo, _, ho = ocg.cg(A, b1, max_iters=K)
+            out.update(apply_err=float(np.max(np.abs(yg - yo) / s)),
+                       dot_rel=abs(bb - ocg.dot(b2, b2)) / ocg.dot(b2, b2),
+                       cg_hist_rel=float(np.max(np.abs(hist - np.array(ho)) / np.array(ho))),
+                       x_rel=float(np.max(np.abs(xgv - xo)) / np.max(np.abs(xo))), iterations=j)
+            out["ok"] = out["apply_err"] <= 1e-12 and out["cg_hist_rel"] <= 1e-8 and out["x_rel"] <= 1e-10
+    except Exception as ex:
+        out["error"] = repr(ex)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
