@@ -34,6 +34,7 @@ def _compile(src: str, nccl: str, extra: list[str]) -> str:
     cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
            "-Xptxas", "-v" if os.environ.get("HB_PTXAS_V") else "-O3",
+           *(["-DHB_TUNE"] if os.environ.get("HB_TUNE") else []),
            *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -50,7 +51,8 @@ def build(force: bool = False, extra: list[str] | None = None) -> str:
     hdrs.append(os.path.join(ROOT, "include", "hipbone_b200.h"))
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
-        if all(os.path.getmtime(f) < t for f in srcs + hdrs + [__file__]):
+        stamp = os.path.join(LIBDIR, ".tune" if os.environ.get("HB_TUNE") else ".plain")
+        if all(os.path.getmtime(f) < t for f in srcs + hdrs + [__file__]) and os.path.exists(stamp):
             return LIB
     nccl = nccl_root()
     with ThreadPoolExecutor(len(SOURCES)) as ex:
@@ -62,6 +64,10 @@ def build(force: bool = False, extra: list[str] | None = None) -> str:
         raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     for o in objs:
         os.remove(o)
+    for st in (".tune", ".plain"):
+        if os.path.exists(os.path.join(LIBDIR, st)):
+            os.remove(os.path.join(LIBDIR, st))
+    open(os.path.join(LIBDIR, ".tune" if os.environ.get("HB_TUNE") else ".plain"), "w").close()
     return LIB
 
 

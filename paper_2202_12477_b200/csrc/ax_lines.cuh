@@ -38,8 +38,10 @@ struct LinesShape {
   static constexpr int NP = N + 1;
   static constexpr int NP2 = NP * NP;
   static constexpr int NP3 = NP2 * NP;
-  // ~64 threads per CTA (one element from N = 7 up): fine-grained CTAs balance best
-  static constexpr int EPB = EPBX > 0 ? EPBX : ((64 / NP2) > 0 ? (64 / NP2) : 1);
+  // ~64 threads per CTA (one element from N = 7 up): fine-grained CTAs balance best; N = 5
+  // measured best with ~128 (profiles/r1_tune.jsonl)
+  static constexpr int EPB_DEF = N == 5 ? 128 / NP2 : ((64 / NP2) > 0 ? (64 / NP2) : 1);
+  static constexpr int EPB = EPBX > 0 ? EPBX : EPB_DEF;
   static constexpr int BLOCK = EPB * NP2;
   // Shared-memory layout of one element buffer: (i,j,k) -> doubles.  NP = 8 and NP = 16 use an
   // XOR swizzle that makes all three line orientations conflict free; other N use row / layer
@@ -64,14 +66,14 @@ struct LinesShape {
   static constexpr int CONST = 2 * MAT;               // D and D^T (host-built, g_EO[N])
   static_assert(CONST <= EO_MAX, "folded D table");
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
-  // resident CTAs per SM requested from ptxas: ~96 (N <= 6) / 128 registers per thread
-  // (enough for the line arrays), capped by the shared-memory footprint and 32 CTAs/SM
-  static constexpr int REGS = N <= 6 ? 96 : 128;
-  static constexpr int MINB_REG0 = 65536 / (BLOCK * REGS);
+  // Resident CTAs per SM requested from ptxas, from a per-N register target measured on the
+  // B200 (profiles/r1_tune.jsonl; 0 = no cap, one CTA per SM), capped by shared memory.
+  static constexpr int REGS_T[16] = {0, 64, 64, 64, 96, 96, 128, 128, 128, 128, 128, 128, 0, 128, 0, 0};
+  static constexpr int REGS = REGS_T[N];
+  static constexpr int MINB_REG0 = REGS ? 65536 / (BLOCK * REGS) : 1;
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
-  // N >= 12: one 256-thread CTA per SM without a register cap measured best (no spills)
-  static constexpr int MINB = N >= 12 ? 1 : (MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM));
+  static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
 };
 
 // sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs

@@ -110,29 +110,63 @@ AxKernel pick_ax_n(bool halo, bool massb) {
 }
 
 // experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
-AxKernel pick_ax_variant(int N, int v) {
-  if (N == 15) {
-    switch (v) {
-      case 1: return make_lines<15, false, false, 0, 1>();                      // no register cap
-      case 2: return make_lines<15, false, false, 0, 2, 0, false>();            // no G prefetch
-      case 3: return make_lines<15, false, false, 0, 2, 0, true, false>();      // G cached normally
-      case 4: return make_lines<15, false, false, 0, 1, 0, false>();            // no cap, no prefetch
-      default: return make_lines<15, false, false, kLinesPF>();
-    }
-  }
+#ifdef HB_TUNE
+// Tuning build (-DHB_TUNE): per-N launch-shape variants selected with HB_AX_VN / HB_AX_VARIANT.
+template <int N, int EPBX, int REGS>
+constexpr int tune_minb() {
+  using S = hbk::LinesShape<N, EPBX>;
+  int r = 65536 / (S::BLOCK * REGS);
+  int m = (int)((227 * 1024) / (S::SMEM + 1024));
+  r = r < m ? r : m;
+  r = r > 16 ? 16 : r;
+  return r < 1 ? 1 : r;
+}
+
+template <int N>
+AxKernel tune_variant(int v) {
+  constexpr int NP2 = (N + 1) * (N + 1);
+  constexpr int E128 = 128 / NP2 > 0 ? 128 / NP2 : 1;
+  constexpr int E256 = 256 / NP2 > 0 ? 256 / NP2 : 1;
   switch (v) {
-    case 1: return make_lines<7, false, false, 0, 8, 0, true, false>();   // G cached normally
-    case 2: return make_lines<7, false, false, 0, 8, 0, false>();         // no L2 prefetch of G
-    default: return make_lines<7, false, false, kLinesPF>();
+    case 1: return make_lines<N, false, false, 0, tune_minb<N, E128, 96>(), E128>();
+    case 2: return make_lines<N, false, false, 0, tune_minb<N, E256, 96>(), E256>();
+    case 3: return make_lines<N, false, false, 0, tune_minb<N, 0, 64>()>();
+    case 4: return make_lines<N, false, false, 0, 1>();
+    case 5: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>()>();
+    case 6: return make_lines<N, false, false, 0, tune_minb<N, E128, 128>(), E128>();
+    default: return make_lines<N, false, false, kLinesPF>();
   }
 }
 
+AxKernel pick_ax_variant(int N, int v) {
+  switch (N) {
+    case 1: return tune_variant<1>(v);
+    case 2: return tune_variant<2>(v);
+    case 3: return tune_variant<3>(v);
+    case 4: return tune_variant<4>(v);
+    case 5: return tune_variant<5>(v);
+    case 6: return tune_variant<6>(v);
+    case 7: return tune_variant<7>(v);
+    case 8: return tune_variant<8>(v);
+    case 9: return tune_variant<9>(v);
+    case 10: return tune_variant<10>(v);
+    case 11: return tune_variant<11>(v);
+    case 12: return tune_variant<12>(v);
+    case 13: return tune_variant<13>(v);
+    case 14: return tune_variant<14>(v);
+    default: return tune_variant<15>(v);
+  }
+}
+#endif
+
 AxKernel pick_ax(int N, bool halo, bool massb) {
-  if ((N == 7 || N == 15) && !halo && !massb) {
+#ifdef HB_TUNE
+  if (!halo && !massb) {
     const char* v = getenv("HB_AX_VARIANT");
     const char* vn = getenv("HB_AX_VN");
-    if (v && atoi(v) > 0 && (vn ? atoi(vn) : 7) == N) return pick_ax_variant(N, atoi(v));
+    if (v && atoi(v) > 0 && vn && atoi(vn) == N) return pick_ax_variant(N, atoi(v));
   }
+#endif
   switch (N) {
     case 1: return pick_ax_n<1>(halo, massb);
     case 2: return pick_ax_n<2>(halo, massb);

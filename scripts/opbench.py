@@ -60,13 +60,28 @@ def main():
     ap.add_argument("--box", default="52,52,52")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--tune", default="", help="variants to try per N, e.g. 0,1,2 (needs an HB_TUNE build)")
+    ap.add_argument("--degrees", default="", help="comma list of N for --sweep/--tune (default 1..15)")
     a = ap.parse_args()
     import __graft_entry__
     __graft_entry__.build()
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = json.load(f)["hbm_gbs"]
+    degrees = [int(v) for v in a.degrees.split(",")] if a.degrees else list(C3)
+    if a.tune:
+        for N in degrees:
+            n = C3[N]
+            for v in a.tune.split(","):
+                os.environ["HB_AX_VN"] = str(N)
+                os.environ["HB_AX_VARIANT"] = v
+                try:
+                    run(N, (n, n, n), a.reps, peak)
+                except Exception as ex:  # a variant may not launch (resources): report and go on
+                    print(json.dumps({"N": N, "variant": v, "error": repr(ex)}), flush=True)
+        return
     if a.sweep:
-        for N, n in C3.items():
+        for N in degrees:
+            n = C3[N]
             run(N, (n, n, n), a.reps, peak)
     else:
         run(a.N, tuple(int(v) for v in a.box.split(",")), a.reps, peak)
