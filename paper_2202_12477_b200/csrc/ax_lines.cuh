@@ -215,6 +215,7 @@ ax_lines(const AxArgs a) {
   double* s_D = smem + 3 * EPB * SLAB;  // folded D
   double* s_DT = s_D + S::MAT;          // folded D^T
   for (int q = t; q < S::CONST; q += S::BLOCK) s_D[q] = __ldg(&g_EO[N][q]);  // folded D | D^T
+  pdl_wait();  // everything below may read data written by the previous kernel (PDL launch)
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
   double en = 0.0;  // element energy u.(S_e u) (+ lambda u.B u) of this thread's nodes
 

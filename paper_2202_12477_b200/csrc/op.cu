@@ -246,6 +246,7 @@ struct hb_op {
   DevBuf idx, G, B, owned_gid;
   DevBuf r, p, Ap, xs, partials, e_part, pp_part, scal, hist, dot_out, dot_ticket;
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
+  bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
   std::vector<int32_t> nbr;
   std::vector<int64_t> soff, scnt, roff, rcnt;
@@ -341,7 +342,19 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
     op->prof_used++;
     CU_TRY(record_event(e_start, st));
   }
-  CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
+  if (op->pdl && energy) {
+    // CG iteration (P = 1): programmatic dependent launch -- the operator grid is scheduled
+    // while the previous vector update drains and waits in-kernel (griddepcontrol.wait)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid); cfg.blockDim = dim3(k.block); cfg.dynamicSmemBytes = k.smem; cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    CU_TRY(cudaLaunchKernelExC(&cfg, k.fn, args));
+  } else {
+    CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
+  }
   op->launches++;
   if (timed) CU_TRY(record_event(e_stop, st));
   return HB_OK;
@@ -637,6 +650,10 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
       op->fused_grid = std::min(vec_grid(std::max<int64_t>(n, 1)), nb * num_sms());
   }
   HB_TRY(op->pp_part.alloc((size_t)std::max(op->fused_grid, 1) * 8 + 64));
+  {
+    const char* env = getenv("HB_PDL");
+    op->pdl = op->fused_grid > 0 && !(env && env[0] == '0');
+  }
   if (m->P > 1 && comm) {
     int lo, hi;
     CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -746,8 +763,15 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
     double* rrp = op->partials.as<double>();
     double* hp = op->hist.as<double>();
     void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &ppp, &lpp, &li, &rrp, &s, &hp};
-    CU_TRY(cudaLaunchCooperativeKernel((const void*)&hbk::cg_update_fused, dim3(op->fused_grid),
-                                       dim3(hbk::VEC_BLOCK), args, 0, st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(op->fused_grid); cfg.blockDim = dim3(hbk::VEC_BLOCK); cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at; cfg.numAttrs = op->pdl ? 2 : 1;
+    CU_TRY(cudaLaunchKernelExC(&cfg, (const void*)&hbk::cg_update_fused, args));
     op->launches++;
     return phase_event(op, op->t_xr, false, st);
   }

@@ -177,6 +177,7 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
                 double lam_init, double* rr_part, CgScalars* s, double* hist) {
   __shared__ double s_b[2];
+  pdl_wait();
   // ---- p.Ap and alpha (identical in every CTA)
   double ev = 0.0, pv_ = 0.0;
   for (int b = threadIdx.x; b < n_epart; b += VEC_BLOCK) ev += e_part[b];

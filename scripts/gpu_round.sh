@@ -13,7 +13,8 @@ for s in $STAGES; do
     smoke) timeout 300 python __graft_entry__.py smoke > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status.txt ;;
     bench) timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/status.txt
            timeout 900 python bench.py --box 52,52,52 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_c3n7.json 2>> $O/bench.err; echo "bench c3 rc=$?" >> $O/status.txt
-           timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2>> $O/bench.err; echo "bench ref rc=$?" >> $O/status.txt ;;
+           timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2>> $O/bench.err; echo "bench ref rc=$?" >> $O/status.txt
+           HB_PDL=0 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_nopdl.json 2>> $O/bench.err; echo "bench nopdl rc=$?" >> $O/status.txt ;;
     var) : > $O/opbench_variants.jsonl
          for v in $VARIANTS; do
            HB_AX_VARIANT=$v timeout 300 python scripts/opbench.py --N 7 --box 52,52,52 >> $O/opbench_variants.jsonl 2>> $O/opbench.err
