@@ -149,7 +149,9 @@ int hb_dot(hb_op* op, const double* a_dev, const double* b_dev, double* out_host
 /* CG (Alg. 1) from x_0 = 0 (c13).  eps < 0: fixed mode, exactly max_iters
  * iterations, captured in a CUDA graph; eps >= 0: tolerance mode, stop when
  * r.r <= eps (absolute, c14) or j == max_iters; HB_ERR_BREAKDOWN if p.Ap <= 0 or
- * non-finite.  rr_hist_host (nullable) receives r_j.r_j for j = 0..iterations
+ * non-finite.  With P = 1 tolerance mode is also one CUDA graph: a WHILE conditional node
+ * whose loop test (r.r > eps, j < max_iters, no breakdown) runs on the device, so the host
+ * synchronises only at the end (env HB_TOL_GRAPH=0 selects a host-driven loop).  rr_hist_host (nullable) receives r_j.r_j for j = 0..iterations
  * ([max_iters+1]).  x_dev receives the solution [n_owned].  Synchronises the stream at the end. */
 int hb_cg_solve(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters, double eps,
                 double* rr_hist_host, hb_cg_result* res, void* stream);

@@ -22,7 +22,7 @@ struct CgScalars {
   int32_t it;        // iteration counter j
   uint32_t ticket;   // last-CTA detection, vector kernels
   uint32_t ticket_e; // last-CTA detection, operator energy
-  int32_t pad2;
+  int32_t flags;     // bit 0: CG breakdown detected on the device (tolerance-mode graph)
 };
 
 struct AxArgs {

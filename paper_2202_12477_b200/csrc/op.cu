@@ -255,6 +255,7 @@ struct hb_op {
   AxKernel ax_plain, ax_halo;
   cudaStream_t comm_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture (the legacy stream cannot be captured)
+  cudaStream_t cap_stream2 = nullptr; // captures the body of the tolerance-mode WHILE node
   cudaEvent_t ev_cap = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_haloel = nullptr, ev_gather = nullptr;
   cudaEvent_t ev_red = nullptr, ev_red_done = nullptr;
@@ -279,6 +280,11 @@ struct hb_op {
   };
   struct GraphVal { cudaGraphExec_t exec; int64_t launches; size_t prof_events, prof_xr, prof_p; };
   std::map<GraphKey, GraphVal> graphs;
+  struct TolKey {
+    int32_t K; const double* b; double* x; double eps; cudaStream_t st;
+    bool operator<(const TolKey& o) const { return std::tie(K, b, x, eps, st) < std::tie(o.K, o.b, o.x, o.eps, o.st); }
+  };
+  std::map<TolKey, GraphVal> tol_graphs;  // tolerance mode, one CUDA graph with a WHILE node
   double* host_scal = nullptr;  // pinned CgScalars mirror
   ~hb_op() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -287,6 +293,8 @@ struct hb_op {
       for (auto& pr : tm->ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (cap_stream2) cudaStreamDestroy(cap_stream2);
+    for (auto& kv : tol_graphs) cudaGraphExecDestroy(kv.second.exec);
     if (ev_cap) cudaEventDestroy(ev_cap);
     for (cudaEvent_t e : {ev_pack, ev_halo, ev_haloel, ev_gather, ev_red, ev_red_done}) if (e) cudaEventDestroy(e);
     if (host_scal) cudaFreeHost(host_scal);
@@ -660,6 +668,7 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     CU_TRY(cudaStreamCreateWithPriority(&op->comm_stream, cudaStreamNonBlocking, hi));
   }
   CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
+  CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream2, cudaStreamNonBlocking));
   for (cudaEvent_t* e : {&op->ev_pack, &op->ev_halo, &op->ev_haloel, &op->ev_gather, &op->ev_red, &op->ev_red_done, &op->ev_cap})
     CU_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CU_TRY(cudaStreamSynchronize(st));
@@ -829,6 +838,8 @@ int ensure_hist(hb_op* op, int32_t K) {
     // graphs reference the old history buffer
     for (auto& kv : op->graphs) cudaGraphExecDestroy(kv.second.exec);
     op->graphs.clear();
+    for (auto& kv : op->tol_graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->tol_graphs.clear();
     HB_TRY(op->hist.alloc(need));
   }
   return HB_OK;
@@ -880,6 +891,94 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
   return finish_result(op, K, rr_hist_host, res, st);
 }
 
+// Tolerance mode fully on the device (P = 1): one CUDA graph
+//   init -> cg_continue(first) -> WHILE(cond) { operator ; fused vector update ; cg_continue }
+// captured once per (K, b, x, eps) and replayed; the host synchronises only at the end.
+int cg_tol_graph(hb_op* op, const double* b, double* x, int32_t max_iters, double eps, double* rr_hist_host,
+                 hb_cg_result* res, cudaStream_t st) {
+  HB_TRY(ensure_hist(op, max_iters));
+  hb_op::TolKey key{max_iters, b, x, eps, st};
+  auto it = op->tol_graphs.find(key);
+  if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }
+  if (it == op->tol_graphs.end()) {
+    const int64_t l0 = op->launches;
+    const bool prof = op->profiling;
+    op->profiling = false;  // a data-dependent trip count cannot own a fixed event set
+    cudaStream_t cs = op->cap_stream, cs2 = op->cap_stream2;
+    hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
+    cudaGraph_t graph = nullptr;
+    int status = HB_OK;
+    auto fail = [&](cudaError_t e, const char* what) {
+      if (e != cudaSuccess && status == HB_OK) {
+        (void)cudaGetLastError();
+        set_error(std::string("cg_tol_graph: ") + what + ": " + cudaGetErrorString(e));
+        status = HB_ERR_CUDA;
+      }
+    };
+    fail(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+    if (status == HB_OK) status = cg_init(op, b, x, cs);
+    cudaGraphConditionalHandle h = 0;
+    cudaGraph_t cap_graph = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaStreamCaptureStatus cst;
+    if (status == HB_OK) fail(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cap_graph, &deps, &ndeps), "capture info");
+    if (status == HB_OK) fail(cudaGraphConditionalHandleCreate(&h, cap_graph, 0, 0), "conditional handle");
+    if (status == HB_OK) {
+      hbk::cg_continue<<<1, 1, 0, cs>>>(h, s, eps, max_iters, 1);
+      fail(cudaGetLastError(), "cg_continue");
+    }
+    cudaGraphNode_t cond = nullptr;
+    cudaGraph_t body = nullptr;
+    if (status == HB_OK) fail(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cap_graph, &deps, &ndeps), "capture info");
+    if (status == HB_OK) {
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      fail(cudaGraphAddNode(&cond, cap_graph, deps, ndeps, &cp), "add WHILE node");
+      if (status == HB_OK) body = cp.conditional.phGraph_out[0];
+    }
+    if (status == HB_OK) fail(cudaStreamUpdateCaptureDependencies(cs, &cond, 1, cudaStreamSetCaptureDependencies),
+                              "update capture deps");
+    if (status == HB_OK) {  // loop body on a second stream captured into the WHILE node's graph
+      fail(cudaStreamBeginCaptureToGraph(cs2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+           "begin body capture");
+      if (status == HB_OK) {
+        status = cg_iteration(op, x, cs2);
+        if (status == HB_OK) {
+          hbk::cg_continue<<<1, 1, 0, cs2>>>(h, s, eps, max_iters, 0);
+          fail(cudaGetLastError(), "cg_continue");
+        }
+        cudaGraph_t bg = nullptr;
+        fail(cudaStreamEndCapture(cs2, &bg), "end body capture");
+      }
+    }
+    cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+    op->profiling = prof;
+    if (status != HB_OK) { if (ce == cudaSuccess && graph) cudaGraphDestroy(graph); return status; }
+    CU_TRY(ce);
+    cudaGraphExec_t exec;
+    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CU_TRY(ie);
+    it = op->tol_graphs.emplace(key, hb_op::GraphVal{exec, op->launches - l0, 0, 0, 0}).first;
+    op->launches = l0;
+  }
+  CU_TRY(cudaGraphLaunch(it->second.exec, st));
+  CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  const hbk::CgScalars* hs = reinterpret_cast<const hbk::CgScalars*>(op->host_scal);
+  const int32_t iters = hs->it;
+  op->launches += 1 + (int64_t)iters * 3;  // init + (operator, update, loop test) per trip
+  if (hs->flags & 1) {
+    set_error("hb_cg_solve: breakdown (p.Ap <= 0 or non-finite) at iteration " + std::to_string(iters - 1));
+    return HB_ERR_BREAKDOWN;
+  }
+  return finish_result(op, iters, rr_hist_host, res, st);
+}
+
 int cg_tol(hb_op* op, const double* b, double* x, int32_t max_iters, double eps, double* rr_hist_host,
            hb_cg_result* res, cudaStream_t st) {
   HB_TRY(ensure_hist(op, max_iters));
@@ -914,6 +1013,8 @@ extern "C" int hb_cg_solve(hb_op* op, const double* b, double* x, int32_t max_it
   HB_TRY(check_multi(op, "hb_cg_solve"));
   cudaStream_t st = (cudaStream_t)stream;
   if (eps < 0) return cg_fixed(op, b, x, max_iters, rr_hist_host, res, st);
+  const char* env = getenv("HB_TOL_GRAPH");
+  if (op->fused_grid > 0 && !(env && env[0] == '0')) return cg_tol_graph(op, b, x, max_iters, eps, rr_hist_host, res, st);
   return cg_tol(op, b, x, max_iters, eps, rr_hist_host, res, st);
 }
 

@@ -330,6 +330,20 @@ cg_update_p(double* __restrict__ p, const double* __restrict__ r, double* __rest
   }
 }
 
+// Device-side loop test of the tolerance-mode graph (Alg. 1 line 6: while r.r > eps), with
+// the iteration cap and the breakdown check (p.Ap <= 0 or non-finite) folded in; sets the
+// WHILE node's condition so the solve runs without host round trips.
+__global__ void cg_continue(cudaGraphConditionalHandle h, CgScalars* s, double eps, int32_t max_iters, int first) {
+  bool go = s->rr_new > eps && s->it < max_iters;
+  if (!first) {
+    const bool brk = !(s->pAp > 0.0) || !isfinite(s->pAp) || !isfinite(s->rr_new);
+    if (brk) { s->flags |= 1; go = false; }
+  } else {
+    s->flags = 0;
+  }
+  cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
 // generic dot a.b -> *out (used by hb_dot)
 __global__ void __launch_bounds__(VEC_BLOCK)
 vec_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partials,

@@ -376,3 +376,34 @@ def test_loopback_uneven_partitions_cg(hb, box, N, P):
     j2, h2 = g.cg(bs, xs2, jo)
     assert j2 == jo
     _cg_contract(h2, ho, jo - 1)
+
+
+def test_tolerance_mode_device_graph_matches_host_loop(hb, monkeypatch):
+    """Tolerance mode as one CUDA graph with a WHILE node (device-side loop test, NEXT #1)
+    against the host-driven loop: same iteration count, histories equal to c18 tolerance,
+    and the oracle's stop index."""
+    box, N = (6, 5, 4), 5
+    o = OracleProblem(box, N)
+    bo = of.forcing(range(o.NG), 1)
+    eps = 1e-16 * ocg.dot(bo, bo)
+    xo, jo, ho = ocg.cg(lambda v: o.apply(v, 1.0), bo, max_iters=200, eps=eps)
+    m = hb.Mesh(*box, N)
+    op = hb.Operator(m)
+    b = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.forcing(1, b)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("HB_TOL_GRAPH", mode)
+        x = torch.zeros_like(b)
+        for rep in range(2):  # second run replays the cached graph
+            j, h = op.cg(b, x, 200, eps)
+        res[mode] = (j, h, x.cpu().numpy())
+    assert res["1"][0] == res["0"][0] == jo
+    _cg_contract(res["1"][1], ho, jo - 1)
+    _cg_contract(res["0"][1], ho, jo - 1)
+    assert np.abs(res["1"][2] - xo).max() <= 1e-10 * np.abs(xo).max()
+    # max_iters caps the device loop
+    monkeypatch.setenv("HB_TOL_GRAPH", "1")
+    x = torch.zeros_like(b)
+    j, h = op.cg(b, x, 7, eps)
+    assert j == 7 and len(h) == 8
