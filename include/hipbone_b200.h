@@ -159,6 +159,14 @@ int hb_cg_solve(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters
  * x back; copies are inside the call (end-to-end path). */
 int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t max_iters, double eps,
                      double* rr_hist_host, hb_cg_result* res, void* stream);
+/* Jacobi-preconditioned CG (NekBone's diagonal preconditioner, P:140 --
+ * hipBone itself uses none).  enable = 1 computes M = diag(A) on the device once
+ * (sum over slots of (S_L^e)_nn, + lambda) and makes hb_cg_solve run PCG: alpha = r.z / p.Ap,
+ * beta = r'.z' / r.z, p = z + beta p with z = M^-1 r; the stopping test stays r.r <= eps and
+ * the history stays r.r.  P = 1 only (HB_ERR_STATE otherwise).  Synchronous.
+ * hb_op_jacobi_diagonal writes diag(A) [n_owned] to a device buffer (test hook). */
+int hb_op_set_jacobi(hb_op* op, int enable, void* stream);
+int hb_op_jacobi_diagonal(hb_op* op, double* diag_dev, void* stream);
 /* Profiling of the operator kernel inside hb_cg_solve / hb_op_apply: enable = k > 0 brackets
  * every k-th operator launch with CUDA events on its stream (inside captured graphs as event
  * nodes); enable = 0 turns it off.  hb_op_kernel_time returns the number of timed launches

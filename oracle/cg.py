@@ -45,3 +45,36 @@ def cg(apply_A, b: np.ndarray, *, max_iters: int, eps: float | None = None):
         hist.append(rr)
         j += 1
     return x, j, hist
+
+
+def pcg(apply_A, b: np.ndarray, minv: np.ndarray, *, max_iters: int, eps: float | None = None):
+    """Preconditioned CG (textbook form, e.g. Saad, Iterative Methods, Alg. 9.1) with a
+    diagonal preconditioner M^-1 = diag(minv) -- NekBone's "simple diagonal preconditioning"
+    (hipBone itself has none).  Alg. 1 with z = M^-1 r:
+        alpha = r.z / p.Ap ; x += alpha p ; r -= alpha Ap ; z = M^-1 r
+        beta = r'.z' / r.z ; p = z + beta p
+    The stopping test stays Alg. 1's r.r > eps; the history records r.r.
+    Returns (x, j, rr_history)."""
+    x = np.zeros_like(b)
+    r = b - apply_A(x)
+    z = minv * r
+    p = z.copy()
+    rz = dot(r, z)
+    rr = dot(r, r)
+    hist = [rr]
+    j = 0
+    while j < max_iters and (eps is None or rr > eps):
+        Ap = apply_A(p)
+        pAp = dot(p, Ap)
+        alpha = rz / pAp if pAp != 0.0 else 0.0
+        x = x + alpha * p
+        r = r - alpha * Ap
+        z = minv * r
+        rz_new = dot(r, z)
+        beta = rz_new / rz if rz != 0.0 else 0.0
+        p = z + beta * p
+        rz = rz_new
+        rr = dot(r, r)
+        hist.append(rr)
+        j += 1
+    return x, j, hist

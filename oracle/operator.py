@@ -175,3 +175,12 @@ def apply_entries(x_of, gids, nx, ny, nz, N, D, G_of, lam, M_of, l2g_fn):
                 total += y[n]
         out[t] = total
     return out
+
+
+def diagonal(gid: np.ndarray, NG: int, D: np.ndarray, G: np.ndarray, lam: float, M: np.ndarray) -> np.ndarray:
+    """diag(A) = Z^T diag(S_L^e + lambda M_e) (the Jacobi preconditioner of NEXT #3): the
+    diagonal of every explicit element matrix, assembled (tiny meshes)."""
+    d = np.zeros(gid.shape)
+    for e in range(gid.shape[0]):
+        d[e] = np.diag(element_matrix(D, G[e])) + lam * M[e]
+    return assemble(gid, d, NG)

@@ -18,7 +18,8 @@ struct CgScalars {
   double rr_new;   // r_{j+1}.r_{j+1} (global after allreduce)
   double pp;       // local p.p (for the lambda term of the fused p.Ap)
   double e_acc;    // element-energy accumulator across the operator launches of one apply
-  double pad[3];
+  double rz;       // Jacobi PCG: r_j.z_j (z = M^-1 r), the rho of alpha / beta
+  double pad[2];
   int32_t it;        // iteration counter j
   uint32_t ticket;   // last-CTA detection, vector kernels
   uint32_t ticket_e; // last-CTA detection, operator energy

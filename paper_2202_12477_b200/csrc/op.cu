@@ -244,7 +244,8 @@ struct hb_op {
   // device data
   DevBuf arena;  // [idx | r | p | Ap | xs]: the data every CG iteration re-reads besides G
   DevBuf idx, G, B, owned_gid;
-  DevBuf r, p, Ap, xs, partials, e_part, pp_part, scal, hist, dot_out, dot_ticket;
+  DevBuf r, p, Ap, xs, partials, e_part, pp_part, rz_part, invd, scal, hist, dot_out, dot_ticket;
+  bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
   bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
@@ -658,6 +659,7 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
       op->fused_grid = std::min(vec_grid(std::max<int64_t>(n, 1)), nb * num_sms());
   }
   HB_TRY(op->pp_part.alloc((size_t)std::max(op->fused_grid, 1) * 8 + 64));
+  HB_TRY(op->rz_part.alloc((size_t)std::max(op->fused_grid, 1) * 8 + 64));
   {
     const char* env = getenv("HB_PDL");
     op->pdl = op->fused_grid > 0 && !(env && env[0] == '0');
@@ -745,7 +747,8 @@ int cg_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
   const bool fused = op->fused_grid > 0;
   hbk::cg_init<<<fused ? op->fused_grid : vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
       b, x, op->r.as<double>(), op->p.as<double>(), op->Ap.as<double>(), n, lam_init(op),
-      op->partials.as<double>(), op->scal.as<hbk::CgScalars>(), fused ? op->pp_part.as<double>() : nullptr);
+      op->partials.as<double>(), op->scal.as<hbk::CgScalars>(), fused ? op->pp_part.as<double>() : nullptr,
+      op->jacobi ? op->invd.as<double>() : nullptr);
   op->launches++;
   CU_TRY(cudaGetLastError());
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
@@ -771,7 +774,9 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
     double lpp = lam_pp(op), li = lam_init(op);
     double* rrp = op->partials.as<double>();
     double* hp = op->hist.as<double>();
-    void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &ppp, &lpp, &li, &rrp, &s, &hp};
+    const double* ivd = op->jacobi ? op->invd.as<double>() : nullptr;
+    double* rzp = op->rz_part.as<double>();
+    void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &ppp, &lpp, &li, &rrp, &s, &hp, &ivd, &rzp};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(op->fused_grid); cfg.blockDim = dim3(hbk::VEC_BLOCK); cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -1030,6 +1035,46 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
   HB_TRY(hb_cg_solve(op, b_dev, op->xs.as<double>(), max_iters, eps, rr_hist_host, res, stream));
   if (bytes) CU_TRY(cudaMemcpyAsync(x_host, op->xs.p, bytes, cudaMemcpyDeviceToHost, st));
   CU_TRY(cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+extern "C" int hb_op_set_jacobi(hb_op* op, int enable, void* stream) {
+  if (!op) { set_error("hb_op_set_jacobi: null pointer"); return HB_ERR_ARG; }
+  if (enable && op->fused_grid <= 0) {
+    set_error("hb_op_set_jacobi: the Jacobi-preconditioned CG is available for P = 1 only");
+    return HB_ERR_STATE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (enable && !op->invd.p) {
+    const int64_t n = op->sz.n_owned, E = op->sz.E_local;
+    HB_TRY(op->invd.alloc((size_t)std::max<int64_t>(n, 1) * 8));
+    CU_TRY(cudaMemsetAsync(op->invd.p, 0, (size_t)n * 8, st));
+    hbk::jacobi_diag_kernel<<<num_sms() * 8, 256, 0, st>>>(op->G.as<double>(), op->idx.as<int32_t>(),
+                                                           op->mass_mode == 1 ? op->B.as<double>() : nullptr, E, op->N,
+                                                           op->lam, op->invd.as<double>());
+    CU_TRY(cudaGetLastError());
+    hbk::invert_kernel<<<num_sms() * 8, 256, 0, st>>>(op->invd.as<double>(), n, op->mass_mode == 0 ? op->lam : 0.0);
+    CU_TRY(cudaGetLastError());
+    op->launches += 2;
+    CU_TRY(cudaStreamSynchronize(st));
+  }
+  if ((enable != 0) != op->jacobi) {  // captured graphs bake the kernel arguments in
+    for (auto& kv : op->graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->graphs.clear();
+    for (auto& kv : op->tol_graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->tol_graphs.clear();
+  }
+  op->jacobi = enable != 0;
+  return HB_OK;
+}
+
+extern "C" int hb_op_jacobi_diagonal(hb_op* op, double* diag_dev, void* stream) {
+  if (!op || (op->sz.n_owned > 0 && !diag_dev)) { set_error("hb_op_jacobi_diagonal: null pointer"); return HB_ERR_ARG; }
+  if (!op->invd.p) { set_error("hb_op_jacobi_diagonal: call hb_op_set_jacobi(op, 1) first"); return HB_ERR_STATE; }
+  const int64_t n = op->sz.n_owned;
+  CU_TRY(cudaMemcpyAsync(diag_dev, op->invd.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  hbk::invert_kernel<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(diag_dev, n, 0.0);
+  CU_TRY(cudaGetLastError());
   return HB_OK;
 }
 

@@ -65,26 +65,36 @@ __device__ __forceinline__ bool finish_reduction(double v, double* partials, uin
   return threadIdx.x == 0;
 }
 
-// r = b; p = b; x = 0; Ap = lam_init * p;  then partial r.r -> rr_new
+// r = b; p = z (= b, or M^-1 b with the Jacobi preconditioner); x = 0; Ap = lam_init * p;
+// global r.r -> rr_new (and r.z -> rz), CTA partials of p.p -> pp_part (fused path)
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_init(const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r,
         double* __restrict__ p, double* __restrict__ Ap, int64_t n, double lam_init,
-        double* partials, CgScalars* s, double* pp_part) {
-  double acc = 0.0;
+        double* partials, CgScalars* s, double* pp_part, const double* __restrict__ invd) {
+  double acc = 0.0, acc_rz = 0.0, acc_pp = 0.0;
   for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK) {
-    double v = b[l];
-    r[l] = v; p[l] = v; x[l] = 0.0; Ap[l] = lam_init * v;
+    const double v = b[l];
+    const double z = invd ? v * invd[l] : v;
+    r[l] = v; p[l] = z; x[l] = 0.0; Ap[l] = lam_init * z;
     acc = fma(v, v, acc);
+    acc_rz = fma(v, z, acc_rz);
+    acc_pp = fma(z, z, acc_pp);
   }
-  if (pp_part) {  // p = r: the CTA partials of p.p for the fused update's first p.Ap
-    const double bs = block_sum(acc);
+  if (pp_part) {  // the CTA partials of p.p for the fused update's first p.Ap
+    const double bs = block_sum(acc_pp);
     if (threadIdx.x == 0) pp_part[blockIdx.x] = bs;
     __syncthreads();
   }
+  if (invd) {  // r.z: ordered two-level sum (its own slice of the partials buffer)
+    double t;
+    if (finish_reduction(acc_rz, partials, &s->ticket, &t)) s->rz = t;
+    __syncthreads();
+  }
   double tot;
-  if (finish_reduction(acc, partials, &s->ticket, &tot)) {
-    s->rr_new = tot;  // allreduced for P > 1
-    s->pp = tot;      // local p.p (p = r)
+  if (finish_reduction(acc, partials + gridDim.x, &s->ticket_e, &tot)) {
+    s->rr_new = tot;        // allreduced for P > 1
+    if (!invd) s->rz = tot;
+    s->pp = tot;            // local p.p for the P > 1 path (no preconditioner there: p = r)
     s->e_acc = 0.0;
     s->it = 0;
   }
@@ -175,8 +185,9 @@ cg_update_xr_e(double* __restrict__ x, const double* __restrict__ p, double* __r
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
-                double lam_init, double* rr_part, CgScalars* s, double* hist) {
-  __shared__ double s_b[2];
+                double lam_init, double* rr_part, CgScalars* s, double* hist, const double* __restrict__ invd,
+                double* rz_part) {
+  __shared__ double s_b[3];
   pdl_wait();
   // ---- p.Ap and alpha (identical in every CTA)
   double ev = 0.0, pv_ = 0.0;
@@ -185,15 +196,17 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
   ev = block_sum(ev);
   __syncthreads();
   pv_ = block_sum(pv_);
-  const double rr = s->rr_new;  // r_j.r_j
+  const double rr = s->rr_new;             // r_j.r_j
+  const double rho = invd ? s->rz : rr;     // r_j.z_j (PCG) or r_j.r_j (CG)
   if (threadIdx.x == 0) s_b[0] = ev + lam_pp * pv_;
   __syncthreads();
   const double pAp = s_b[0];
-  const double alpha = (pAp != 0.0) ? rr / pAp : 0.0;  // c15 guard
-  // ---- x, r update + r.r
+  const double alpha = (pAp != 0.0) ? rho / pAp : 0.0;  // c15 guard
+  // ---- x, r update + r.r (+ r.z)
   const int64_t n2 = n >> 1;
   const int64_t stride = (int64_t)gridDim.x * VEC_BLOCK;
-  double acc = 0.0;
+  double acc = 0.0, acc_rz = 0.0;
+  const double2* d2 = reinterpret_cast<const double2*>(invd);
   {
     double2* x2 = reinterpret_cast<double2*>(x);
     double2* r2 = reinterpret_cast<double2*>(r);
@@ -205,6 +218,10 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       rv.x = fma(-alpha, av.x, rv.x); rv.y = fma(-alpha, av.y, rv.y);
       x2[l] = xv; r2[l] = rv;
       acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
+      if (invd) {
+        const double2 dv = d2[l];
+        acc_rz = fma(rv.x, rv.x * dv.x, acc_rz); acc_rz = fma(rv.y, rv.y * dv.y, acc_rz);
+      }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
       const int64_t l = n - 1;
@@ -212,19 +229,32 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       const double rv = fma(-alpha, Ap[l], r[l]);
       r[l] = rv;
       acc = fma(rv, rv, acc);
+      if (invd) acc_rz = fma(rv, rv * invd[l], acc_rz);
     }
   }
   acc = block_sum(acc);
   if (threadIdx.x == 0) rr_part[blockIdx.x] = acc;
+  if (invd) {
+    __syncthreads();
+    acc_rz = block_sum(acc_rz);
+    if (threadIdx.x == 0) rz_part[blockIdx.x] = acc_rz;
+  }
   cooperative_groups::this_grid().sync();
   // ---- beta (identical in every CTA), p update + p.p
-  double rn = 0.0;
+  double rn = 0.0, zn = 0.0;
   for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) rn += __ldcg(rr_part + b);
   rn = block_sum(rn);
   if (threadIdx.x == 0) s_b[1] = rn;
+  if (invd) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) zn += __ldcg(rz_part + b);
+    zn = block_sum(zn);
+    if (threadIdx.x == 0) s_b[2] = zn;
+  }
   __syncthreads();
   const double rr_new = s_b[1];
-  const double beta = (rr != 0.0) ? rr_new / rr : 0.0;  // c15 guard
+  const double rho_new = invd ? s_b[2] : rr_new;
+  const double beta = (rho != 0.0) ? rho_new / rho : 0.0;  // c15 guard
   double acc2 = 0.0;
   {
     double2* p2 = reinterpret_cast<double2*>(p);
@@ -232,6 +262,10 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
     double2* a2 = reinterpret_cast<double2*>(Ap);
     for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += stride) {
       double2 pv = p2[l], rv = __ldcg(r2 + l);
+      if (invd) {  // z = M^-1 r
+        const double2 dv = d2[l];
+        rv.x *= dv.x; rv.y *= dv.y;
+      }
       pv.x = fma(beta, pv.x, rv.x); pv.y = fma(beta, pv.y, rv.y);
       p2[l] = pv;
       a2[l] = make_double2(lam_init * pv.x, lam_init * pv.y);
@@ -239,7 +273,7 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
       const int64_t l = n - 1;
-      const double pv = fma(beta, p[l], __ldcg(r + l));
+      const double pv = fma(beta, p[l], __ldcg(r + l) * (invd ? invd[l] : 1.0));
       p[l] = pv; Ap[l] = lam_init * pv;
       acc2 = fma(pv, pv, acc2);
     }
@@ -252,6 +286,7 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       s->rr = rr;
       if (hist) hist[s->it] = rr;
       s->rr_new = rr_new;
+      s->rz = rho_new;
       s->it += 1;
     }
   }
@@ -342,6 +377,40 @@ __global__ void cg_continue(cudaGraphConditionalHandle h, CgScalars* s, double e
     s->flags = 0;
   }
   cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+// Jacobi preconditioner (NekBone's "simple diagonal preconditioning",
+// P:140): diag(A)_g = sum over the slots of g of (S_L^e)_nn (+ lambda B_n in mass mode 1);
+// (S_L^e)_nn = sum_m D[m][i]^2 Grr(m,j,k) + D[m][j]^2 Gss(i,m,k) + D[m][k]^2 Gtt(i,j,m)
+//            + 2 D[i][i] D[j][j] Grs + 2 D[i][i] D[k][k] Grt + 2 D[j][j] D[k][k] Gst  (node n).
+// One thread per slot, fp64 RED into diag (setup only).
+__global__ void jacobi_diag_kernel(const double* __restrict__ G, const int32_t* __restrict__ idx,
+                                   const double* __restrict__ B, int64_t E, int N, double lam, double* diag) {
+  const int NP = N + 1, NP2 = NP * NP, NP3 = NP2 * NP;
+  const double* D = c_D[N];
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < E * NP3; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = s / NP3;
+    const int n = (int)(s - e * NP3);
+    const int k = n / NP2, c = n - k * NP2, i = c % NP, j = c / NP;
+    const double* Ge = G + e * 6 * NP3;
+    auto g = [&](int f, int ii, int jj, int kk) { return Ge[(kk * 6 + f) * NP2 + jj * NP + ii]; };
+    double d = 0.0;
+    for (int m = 0; m < NP; ++m) {
+      d += D[m * NP + i] * D[m * NP + i] * g(0, m, j, k);
+      d += D[m * NP + j] * D[m * NP + j] * g(3, i, m, k);
+      d += D[m * NP + k] * D[m * NP + k] * g(5, i, j, m);
+    }
+    const double di = D[i * NP + i], dj = D[j * NP + j], dk = D[k * NP + k];
+    d += 2.0 * (di * dj * g(1, i, j, k) + di * dk * g(2, i, j, k) + dj * dk * g(4, i, j, k));
+    if (B) d += lam * B[s];
+    atomicAdd(diag + idx[s], d);
+  }
+}
+
+// invd = 1 / (diag + shift)   (shift = lambda in mass mode 0: Z^T lambda W Z = lambda I)
+__global__ void invert_kernel(double* __restrict__ d, int64_t n, double shift) {
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n; l += (int64_t)gridDim.x * blockDim.x)
+    d[l] = 1.0 / (d[l] + shift);
 }
 
 // generic dot a.b -> *out (used by hb_dot)

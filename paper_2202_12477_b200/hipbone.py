@@ -84,6 +84,8 @@ _SIGS = {
     "hb_cg_solve": (C.c_int, [_p, _p, _p, C.c_int32, C.c_double, _dp, C.POINTER(hb_cg_result), _p]),
     "hb_cg_solve_host": (C.c_int, [_p, _dp, _dp, C.c_int32, C.c_double, _dp, C.POINTER(hb_cg_result), _p]),
     "hb_op_set_profiling": (C.c_int, [_p, C.c_int]),
+    "hb_op_set_jacobi": (C.c_int, [_p, C.c_int, _p]),
+    "hb_op_jacobi_diagonal": (C.c_int, [_p, _p, _p]),
     "hb_op_kernel_time": (C.c_int, [_p, _i64p, _dp]),
     "hb_op_launch_count": (C.c_int, [_p, _i64p]),
     "hb_op_phase_times": (C.c_int, [_p, _dp]),
@@ -298,6 +300,14 @@ class Operator:
         _check(_lib.hb_cg_solve_host(self._h, _ptr(b, C.c_double), _ptr(x, C.c_double), max_iters, eps,
                                      _ptr(h, C.c_double) if hist else None, C.byref(res), _stream(stream)))
         return res.iterations, (h[:res.iterations + 1].copy() if hist else None)
+
+    def set_jacobi(self, enable: bool, stream=None):
+        """Jacobi-preconditioned CG for subsequent cg() calls (P = 1)."""
+        _check(_lib.hb_op_set_jacobi(self._h, int(bool(enable)), _stream(stream)))
+
+    def jacobi_diagonal(self, out, stream=None):
+        """diag(A) on owned DOFs into the CUDA tensor `out` (after set_jacobi(True))."""
+        _check(_lib.hb_op_jacobi_diagonal(self._h, _dev(out), _stream(stream)))
 
     def set_profiling(self, enable, stride: int = 1):
         """enable=False: off; else time every `stride`-th operator launch with CUDA events."""

@@ -407,3 +407,50 @@ def test_tolerance_mode_device_graph_matches_host_loop(hb, monkeypatch):
     x = torch.zeros_like(b)
     j, h = op.cg(b, x, 7, eps)
     assert j == 7 and len(h) == 8
+
+
+@pytest.mark.parametrize("N,mass_mode", [(3, 0), (5, 1), (7, 0)])
+def test_jacobi_pcg(hb, N, mass_mode, monkeypatch):
+    """Jacobi-preconditioned CG (NEXT #3): diag(A) against the oracle's assembled element
+    diagonals; PCG iterates (fixed and tolerance modes, device-graph and host loops) against
+    the oracle's PCG (c18)."""
+    box = (3, 2, 3)
+    E = int(np.prod(box))
+    xg, w = basis.gll(N)
+    wq = np.einsum("k,j,i->kji", w, w, w).ravel()
+    G = random_spd_factors(E, (N + 1) ** 3, seed=51 + N, scale=wq)
+    B = (random_positive((E, (N + 1) ** 3), 8) * np.exp(2.0 * uniform_vector(E * (N + 1) ** 3, 9)).reshape(E, -1)
+         if mass_mode == 1 else None)
+    o = OracleProblem(box, N, mass_mode=mass_mode, G=G, B=B)
+    d_o = oo.diagonal(o.gid, o.NG, o.D, o.G, 1.0, o.M)
+    m = hb.Mesh(*box, N, mass_mode=mass_mode)
+    m.set_geometry(G)
+    if B is not None:
+        m.set_mass(B)
+    op = hb.Operator(m)
+    op.set_jacobi(True)
+    dg = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.jacobi_diagonal(dg)
+    assert np.max(np.abs(dg.cpu().numpy() - d_o) / d_o) <= 1e-13
+    A = lambda v: o.apply(v, 1.0)
+    bo = of.forcing(range(o.NG), 1)
+    eps = 1e-16 * ocg.dot(bo, bo)
+    xo, jo, ho = ocg.pcg(A, bo, 1.0 / d_o, max_iters=300, eps=eps)
+    b = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.forcing(1, b)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("HB_TOL_GRAPH", mode)
+        x = torch.zeros_like(b)
+        j, h = op.cg(b, x, 300, eps)
+        assert j == jo
+        _cg_contract(h, ho, jo - 1)
+        assert np.abs(x.cpu().numpy() - xo).max() <= 1e-10 * np.abs(xo).max()
+    x = torch.zeros_like(b)
+    jf, hf = op.cg(b, x, jo)
+    _cg_contract(hf, ho, jo - 1)
+    # switching back gives plain CG again
+    op.set_jacobi(False)
+    xc, jc, hc = ocg.cg(A, bo, max_iters=300, eps=eps)
+    x = torch.zeros_like(b)
+    j, h = op.cg(b, x, 300, eps)
+    assert j == jc

@@ -224,3 +224,30 @@ def test_appendix_a_C2_operator_and_tol_cg():
     assert j == a["tol_stop"]
     assert abs(h[1] - a["rr1"]) < 1e-11 * a["rr1"] and abs(h[10] - a["rr10"]) < 1e-10 * a["rr10"]
     assert abs(h[20] - a["rr20"]) < 1e-4 * a["rr20"]
+
+
+@pytest.mark.parametrize("mass_mode", [0, 1])
+def test_diagonal_and_pcg(mass_mode):
+    """Jacobi PCG pins (NEXT #3): oracle diag(A) equals the dense diagonal; PCG with M = I is
+    CG (identical iterates); PCG reaches the direct solution and needs fewer iterations than
+    CG on a problem with a strongly varying mass term."""
+    box, N = (2, 2, 1), 3
+    x, w, D, gid, G, M, NG = setup(box, N, mass_mode=mass_mode)
+    Gr = random_spd_factors(gid.shape[0], (N + 1) ** 3, seed=41, scale=np.einsum("k,j,i->kji", w, w, w).ravel())
+    if mass_mode == 1:
+        M = random_positive(gid.shape, 5) * np.exp(3.0 * uniform_vector(gid.size, 6)).reshape(gid.shape)
+    Ad = operator.dense(gid, NG, D, Gr, 1.0, M)
+    d = operator.diagonal(gid, NG, D, Gr, 1.0, M)
+    assert np.max(np.abs(d - np.diag(Ad))) <= 1e-13 * np.max(np.abs(d))
+    A = lambda v: operator.apply(v, gid, D, Gr, 1.0, M)
+    b = forcing.forcing(range(NG), 1)
+    xa, ja, ha = cg.cg(A, b, max_iters=30)
+    xb, jb, hb_ = cg.pcg(A, b, np.ones(NG), max_iters=30)
+    assert ha == hb_ and np.array_equal(xa, xb)
+    eps = 1e-24 * cg.dot(b, b)
+    xp, jp, hp = cg.pcg(A, b, 1.0 / d, max_iters=1000, eps=eps)
+    xc, jc, hc = cg.cg(A, b, max_iters=1000, eps=eps)
+    xd = np.linalg.solve(Ad, b)
+    assert np.max(np.abs(xp - xd)) <= 1e-9 * np.max(np.abs(xd))
+    if mass_mode == 1:
+        assert jp < jc
