@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-profile", action="store_true", help="do not bracket operator launches with events")
+    ap.add_argument("--variant", type=int, default=0, help="assembly: 0 fused scatter-add, 1 y_L + CSR (P=1)")
+    ap.add_argument("--jacobi", action="store_true", help="Jacobi-preconditioned CG (P=1; not the NekBone FOM)")
     return ap.parse_args()
 
 
@@ -209,6 +211,10 @@ def main():
         box = blk
         mesh = hb.Mesh(*box, N)
     op = hb.Operator(mesh, lam=1.0, comm=comm)
+    if args.variant:
+        op.set_variant(args.variant)
+    if args.jacobi:
+        op.set_jacobi(True)
     s = mesh.sizes
     n = op.n_owned
     E_glob, NG = s["E_global"], s["N_G"]
@@ -323,7 +329,8 @@ def main():
                           "box": list(box), "N": N, "E": E_glob, "N_G": NG, "N_L": E_glob * (N + 1) ** 3,
                           "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
                           "l2": "flushed between steps (256 MiB write); working set > L2",
-                          "parallelism": f"element partition p{world}"},
+                          "parallelism": f"element partition p{world}",
+                          "assembly_variant": args.variant, "preconditioner": "jacobi" if args.jacobi else "none"},
                "gdofs_per_s": round(gdofs, 4),
                "cg_bytes_per_iter_fused": ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3),
                "cg_gbs_fused_ledger": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) * K / (ms * 1e-3) / 1e9, 1),

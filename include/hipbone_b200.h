@@ -159,6 +159,12 @@ int hb_cg_solve(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters
  * x back; copies are inside the call (end-to-end path). */
 int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t max_iters, double eps,
                      double* rr_hist_host, hb_cg_result* res, void* stream);
+/* Assembly variant: 0 (default) = Z^T fused into the operator as fp64 scatter-add (atomic
+ * accumulation order, results reproducible to rounding); 1 = the paper's split form (P:154,
+ * P:219): the operator writes y_L per slot and a CSR gather kernel sums every DOF's slots in
+ * ascending (e, n) order -- bitwise reproducible, +20 N_L bytes per apply.  P = 1 only
+ * (HB_ERR_STATE otherwise).  Synchronous (builds the CSR on first use). */
+int hb_op_set_variant(hb_op* op, int variant, void* stream);
 /* Jacobi-preconditioned CG (NekBone's diagonal preconditioner, P:140 --
  * hipBone itself uses none).  enable = 1 computes M = diag(A) on the device once
  * (sum over slots of (S_L^e)_nn, + lambda) and makes hb_cg_solve run PCG: alpha = r.z / p.Ap,

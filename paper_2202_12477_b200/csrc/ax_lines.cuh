@@ -347,7 +347,9 @@ ax_lines(const AxArgs a) {
           out += lb;
           en = fma(uk, lb, en);
         }
-        if (interior_ij && k > 0 && k < N) {
+        if (a.yL) {  // deterministic variant: y_L per slot, assembled by the CSR gather kernel
+          a.yL[e * NP3 + k * NP2 + c] = out;
+        } else if (interior_ij && k > 0 && k < N) {
           if (!MASSB) out = fma(a.lam, uk, out);  // W = 1 on element-interior nodes
           a.y[gi[k]] = out;                          // sole contribution: plain store
         } else {

@@ -34,6 +34,7 @@ struct AxArgs {
   const double* __restrict__ xh;    // halo values (HALO)
   double* y;                        // owned output (pre-initialised)
   double* yh;                       // halo output accumulator (HALO)
+  double* yL;                       // non-null: deterministic variant, write (S_L + lambda B) u per slot
   int64_t e_begin, e_end;           // element range of this launch
   int32_t n_owned;
   double lam;

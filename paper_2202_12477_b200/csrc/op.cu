@@ -246,6 +246,8 @@ struct hb_op {
   DevBuf idx, G, B, owned_gid;
   DevBuf r, p, Ap, xs, partials, e_part, pp_part, rz_part, invd, scal, hist, dot_out, dot_ticket;
   bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
+  int variant = 0;      // 0: fused scatter-add (fp64 RED); 1: y_L + CSR gather (deterministic), P = 1
+  DevBuf yL, csr_ptr, csr_slots;
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
   bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
@@ -324,6 +326,7 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.xh = op->xh.as<double>();
   a.y = y;
   a.yh = op->yh.as<double>();
+  a.yL = op->variant == 1 ? op->yL.as<double>() : nullptr;
   a.e_begin = e0; a.e_end = e1;
   a.n_owned = (int32_t)op->sz.n_owned;
   a.lam = op->lam;
@@ -489,6 +492,16 @@ int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStrea
   const int64_t E = op->sz.E_local;
   const bool multi = op->comm && op->comm->P > 1;
   if (!multi) {
+    if (op->variant == 1) {  // y_L, then the deterministic CSR gather (adds lambda x in mode 0)
+      HB_TRY(launch_ax(op, op->ax_plain, 0, E, x, y, st, energy, true));
+      const int64_t n = op->sz.n_owned;
+      hbk::csr_gather_kernel<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+          op->csr_ptr.as<int32_t>(), op->csr_slots.as<int32_t>(), op->yL.as<double>(), x,
+          op->mass_mode == 0 ? op->lam : 0.0, y, n);
+      op->launches++;
+      CU_TRY(cudaGetLastError());
+      return HB_OK;
+    }
     HB_TRY(stage_init(op, x, y, init_y, st));
     return launch_ax(op, op->ax_plain, 0, E, x, y, st, energy, true);
   }
@@ -1035,6 +1048,40 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
   HB_TRY(hb_cg_solve(op, b_dev, op->xs.as<double>(), max_iters, eps, rr_hist_host, res, stream));
   if (bytes) CU_TRY(cudaMemcpyAsync(x_host, op->xs.p, bytes, cudaMemcpyDeviceToHost, st));
   CU_TRY(cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
+  if (!op || variant < 0 || variant > 1) { set_error("hb_op_set_variant: bad argument"); return HB_ERR_ARG; }
+  if (variant == 1 && (op->sz.P > 1 || op->comm)) {
+    set_error("hb_op_set_variant: the deterministic y_L + CSR variant is available for P = 1 only");
+    return HB_ERR_STATE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (variant == 1 && !op->yL.p) {
+    // CSR of Z^T over owned DOFs, slots in ascending (e, n) order (counting sort by gid)
+    const int64_t n = op->sz.n_owned, NL = op->sz.N_L;
+    std::vector<int32_t> idx(NL);
+    CU_TRY(cudaMemcpy(idx.data(), op->idx.p, NL * 4, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> ptr(n + 1, 0), slots(NL);
+    for (int64_t t = 0; t < NL; ++t) ptr[idx[t] + 1]++;
+    for (int64_t g = 0; g < n; ++g) ptr[g + 1] += ptr[g];
+    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t t = 0; t < NL; ++t) slots[fill[idx[t]]++] = (int32_t)t;
+    HB_TRY(op->csr_ptr.alloc((n + 1) * 4));
+    HB_TRY(op->csr_slots.alloc(NL * 4));
+    HB_TRY(op->yL.alloc(NL * 8));
+    CU_TRY(cudaMemcpy(op->csr_ptr.p, ptr.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemcpy(op->csr_slots.p, slots.data(), NL * 4, cudaMemcpyHostToDevice));
+  }
+  (void)st;
+  if (variant != op->variant) {
+    for (auto& kv : op->graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->graphs.clear();
+    for (auto& kv : op->tol_graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->tol_graphs.clear();
+  }
+  op->variant = variant;
   return HB_OK;
 }
 

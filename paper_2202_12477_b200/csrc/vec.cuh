@@ -379,6 +379,21 @@ __global__ void cg_continue(cudaGraphConditionalHandle h, CgScalars* s, double e
   cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
+// Deterministic assembly (P:219's gather Z^T through a CSR, K5): y[g] = lam0 x[g] +
+// sum_{t in row g} yL[slot[t]], rows in ascending (e, n) slot order -- a fixed summation
+// order, so the result is bitwise reproducible (the fused variant uses fp64 RED instead).
+__global__ void __launch_bounds__(VEC_BLOCK)
+csr_gather_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ slots,
+                  const double* __restrict__ yL, const double* __restrict__ x, double lam0, double* __restrict__ y,
+                  int64_t n) {
+  for (int64_t g = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; g < n; g += (int64_t)gridDim.x * VEC_BLOCK) {
+    double acc = lam0 * x[g];
+    const int32_t t1 = row_ptr[g + 1];
+    for (int32_t t = row_ptr[g]; t < t1; ++t) acc += yL[slots[t]];
+    y[g] = acc;
+  }
+}
+
 // Jacobi preconditioner (NekBone's "simple diagonal preconditioning",
 // P:140): diag(A)_g = sum over the slots of g of (S_L^e)_nn (+ lambda B_n in mass mode 1);
 // (S_L^e)_nn = sum_m D[m][i]^2 Grr(m,j,k) + D[m][j]^2 Gss(i,m,k) + D[m][k]^2 Gtt(i,j,m)

@@ -85,6 +85,7 @@ _SIGS = {
     "hb_cg_solve_host": (C.c_int, [_p, _dp, _dp, C.c_int32, C.c_double, _dp, C.POINTER(hb_cg_result), _p]),
     "hb_op_set_profiling": (C.c_int, [_p, C.c_int]),
     "hb_op_set_jacobi": (C.c_int, [_p, C.c_int, _p]),
+    "hb_op_set_variant": (C.c_int, [_p, C.c_int, _p]),
     "hb_op_jacobi_diagonal": (C.c_int, [_p, _p, _p]),
     "hb_op_kernel_time": (C.c_int, [_p, _i64p, _dp]),
     "hb_op_launch_count": (C.c_int, [_p, _i64p]),
@@ -300,6 +301,10 @@ class Operator:
         _check(_lib.hb_cg_solve_host(self._h, _ptr(b, C.c_double), _ptr(x, C.c_double), max_iters, eps,
                                      _ptr(h, C.c_double) if hist else None, C.byref(res), _stream(stream)))
         return res.iterations, (h[:res.iterations + 1].copy() if hist else None)
+
+    def set_variant(self, variant: int, stream=None):
+        """0: fused scatter-add (default); 1: y_L + deterministic CSR gather (P = 1)."""
+        _check(_lib.hb_op_set_variant(self._h, int(variant), _stream(stream)))
 
     def set_jacobi(self, enable: bool, stream=None):
         """Jacobi-preconditioned CG for subsequent cg() calls (P = 1)."""

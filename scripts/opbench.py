@@ -25,6 +25,8 @@ def run(N, box, reps, peak):
     from paper_2202_12477_b200 import ledger
     m = hb.Mesh(*box, N)
     op = hb.Operator(m)
+    if int(os.environ.get("HB_BENCH_VARIANT", "0")):
+        op.set_variant(int(os.environ["HB_BENCH_VARIANT"]))
     n = op.n_owned
     s = m.sizes
     x = torch.empty(n, dtype=torch.float64, device="cuda")

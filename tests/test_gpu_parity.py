@@ -454,3 +454,40 @@ def test_jacobi_pcg(hb, N, mass_mode, monkeypatch):
     x = torch.zeros_like(b)
     j, h = op.cg(b, x, 300, eps)
     assert j == jc
+
+
+@pytest.mark.parametrize("N,mass_mode", [(3, 0), (7, 1), (10, 0)])
+def test_deterministic_csr_variant(hb, N, mass_mode):
+    """Assembly variant 1 (y_L + CSR gather in ascending (e, n) order): operator parity
+    (c17), CG parity (c18), and bitwise reproducibility of repeated applies and solves."""
+    box = (3, 3, 2)
+    E = int(np.prod(box))
+    G = random_spd_factors(E, (N + 1) ** 3, seed=61 + N)
+    B = random_positive((E, (N + 1) ** 3), 4) if mass_mode == 1 else None
+    o = OracleProblem(box, N, mass_mode=mass_mode, G=G, B=B)
+    m = hb.Mesh(*box, N, mass_mode=mass_mode)
+    m.set_geometry(G)
+    if B is not None:
+        m.set_mass(B)
+    op = hb.Operator(m)
+    op.set_variant(1)
+    xv = uniform_vector(o.NG, 12)
+    xd = dev(xv)
+    y1 = torch.empty_like(xd)
+    y2 = torch.empty_like(xd)
+    op.apply(xd, y1)
+    op.apply(xd, y2)
+    assert torch.equal(y1, y2)
+    yo = o.apply(xv, 1.0)
+    s = o.scale(xv, 1.0)
+    assert (np.abs(y1.cpu().numpy() - yo) / s).max() <= 1e-12
+    b = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.forcing(1, b)
+    x1, x2 = torch.zeros_like(b), torch.zeros_like(b)
+    j1, h1 = op.cg(b, x1, 30)
+    j2, h2 = op.cg(b, x2, 30)
+    assert np.array_equal(h1, h2) and torch.equal(x1, x2)
+    bo = of.forcing(range(o.NG), 1)
+    xo, jo, ho = ocg.cg(lambda v: o.apply(v, 1.0), bo, max_iters=30)
+    jt = min(30, next((k for k, v in enumerate(ho) if v <= 1e-16 * ho[0]), 30))
+    _cg_contract(h1, ho, jt - 1)
