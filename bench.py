@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="do not bracket operator launches with events")
     ap.add_argument("--variant", type=int, default=0, help="assembly: 0 fused scatter-add, 1 y_L + CSR (P=1)")
     ap.add_argument("--jacobi", action="store_true", help="Jacobi-preconditioned CG (P=1; not the NekBone FOM)")
+    ap.add_argument("--storage", default="assembled", choices=["assembled", "scattered"],
+                    help="scattered = NekBone's x_L storage with weighted dots (P=1 experiment, P:112-121)")
     return ap.parse_args()
 
 
@@ -227,7 +229,10 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
 
     def step():
-        op.cg(b, x, K)
+        if args.storage == "scattered":
+            op.cg_scattered(b, x, K)
+        else:
+            op.cg(b, x, K)
 
     if not args.no_profile:
         # events around every 10th operator launch (inside the CG graph): live kernel timing
@@ -275,22 +280,22 @@ def main():
     xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     bnp, xnp = bh.numpy(), xh.numpy()
     op.set_profiling(False)
-    for _ in range(2):
+    for _ in range(2 if args.storage == "assembled" else 0):
         op.cg_host(bnp, xnp, K, hist=False)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e2e_ms = []
-    for t in range(args.steps):
+    for t in range(args.steps if args.storage == "assembled" else 0):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         op.cg_host(bnp, xnp, K, hist=False)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([sum(e2e_ms) / max(len(e2e_ms), 1)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (e2e_t.item() * 1e-3) / 1e9
+    e2e_fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (e2e_t.item() * 1e-3) / 1e9 if e2e_ms else None
 
     # ---- roofline of the dominant kernel (operator), from the live event timings
     peak, peak_src = peaks()
@@ -330,12 +335,13 @@ def main():
                           "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
                           "l2": "flushed between steps (256 MiB write); working set > L2",
                           "parallelism": f"element partition p{world}",
-                          "assembly_variant": args.variant, "preconditioner": "jacobi" if args.jacobi else "none"},
+                          "assembly_variant": args.variant, "preconditioner": "jacobi" if args.jacobi else "none",
+                          "storage": args.storage},
                "gdofs_per_s": round(gdofs, 4),
                "cg_bytes_per_iter_fused": ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3),
                "cg_gbs_fused_ledger": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) * K / (ms * 1e-3) / 1e9, 1),
-               "e2e": {"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
-                       "d2h_bytes_per_step": 8 * n + 48},
+               "e2e": ({"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
+                        "d2h_bytes_per_step": 8 * n + 48} if e2e_ms else None),
                "gpu_launches": launches,
                "phase_ms_per_iter": ({"operator": round(1e3 * sum(p[0] for p in phases) / len(phases), 4),
                                       "xr_update": round(1e3 * sum(p[1] for p in phases) / len(phases), 4),

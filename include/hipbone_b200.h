@@ -155,6 +155,14 @@ int hb_dot(hb_op* op, const double* a_dev, const double* b_dev, double* out_host
  * ([max_iters+1]).  x_dev receives the solution [n_owned].  Synchronises the stream at the end. */
 int hb_cg_solve(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters, double eps,
                 double* rr_hist_host, hb_cg_result* res, void* stream);
+/* NekBone's scattered storage, for comparison with the
+ * assembled storage above: CG on local vectors x_L = Z x of length N_L with the operator
+ * (Z Z^T S_L + lambda I) x_L (element kernel on x_L, combined gather-scatter through a CSR
+ * in ascending (e, n) order) and inner products weighted by the inverse counting vector W
+ * (P:121).  Same arguments and modes as hb_cg_solve (b, x assembled [n_owned]); P = 1 and
+ * mass mode 0 only (HB_ERR_STATE otherwise).  Synchronises the stream at the end. */
+int hb_cg_solve_scattered(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters, double eps,
+                          double* rr_hist_host, hb_cg_result* res, void* stream);
 /* Same solve with HOST buffers: copies b (pinned or pageable) to the device, solves, copies
  * x back; copies are inside the call (end-to-end path). */
 int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t max_iters, double eps,

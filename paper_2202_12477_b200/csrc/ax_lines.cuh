@@ -198,8 +198,10 @@ __device__ __forceinline__ double ldG(const double* p) {
   else return __ldg(p);
 }
 
+// ASM: 0 = fused scatter-add into assembled storage (fp64 RED / store); 1 = write y_L per slot
+// (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L.
 template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0, bool PFL = true,
-          bool GCS = true>
+          bool GCS = true, int ASM = 0>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
@@ -215,7 +217,6 @@ ax_lines(const AxArgs a) {
   double* s_D = smem + 3 * EPB * SLAB;  // folded D
   double* s_DT = s_D + S::MAT;          // folded D^T
   for (int q = t; q < S::CONST; q += S::BLOCK) s_D[q] = __ldg(&g_EO[N][q]);  // folded D | D^T
-  pdl_wait();  // everything below may read data written by the previous kernel (PDL launch)
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
   double en = 0.0;  // element energy u.(S_e u) (+ lambda u.B u) of this thread's nodes
 
@@ -266,10 +267,11 @@ ax_lines(const AxArgs a) {
     {
       double col[1][NP];
 #pragma unroll
-      for (int k = 0; k < NP; ++k) gi[k] = act ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
+      for (int k = 0; k < NP; ++k) gi[k] = (act && ASM != 2) ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
+        if constexpr (ASM == 2) col[0][k] = act ? __ldg(a.xh + e * NP3 + k * NP2 + c) : 0.0;  // x_L
+        else col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
         s_u[S::at(ca, cb, k)] = col[0][k];
       }
       eo_apply<N, EPBX, 1>(s_D, col, gt);
@@ -347,8 +349,8 @@ ax_lines(const AxArgs a) {
           out += lb;
           en = fma(uk, lb, en);
         }
-        if (a.yL) {  // deterministic variant: y_L per slot, assembled by the CSR gather kernel
-          a.yL[e * NP3 + k * NP2 + c] = out;
+        if constexpr (ASM >= 1) {  // y_L per slot, assembled by a CSR (gather-scatter) kernel
+          a.yh[e * NP3 + k * NP2 + c] = out;  // y_L
         } else if (interior_ij && k > 0 && k < N) {
           if (!MASSB) out = fma(a.lam, uk, out);  // W = 1 on element-interior nodes
           a.y[gi[k]] = out;                          // sole contribution: plain store

@@ -91,10 +91,10 @@ struct AxKernel {
 };
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0, bool PFL = true,
-          bool GCS = true>
+          bool GCS = true, int ASM = 0>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
@@ -104,12 +104,16 @@ AxKernel make_lines() {
 constexpr int kLinesPF = 0;  // L2 bulk prefetch distance (grid waves); measured slower on B200
 
 template <int N>
-AxKernel pick_ax_n(bool halo, bool massb) {
+AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
+  constexpr int M = hbk::LinesShape<N>::MINB;
   if (halo) return massb ? make_lines<N, true, true, kLinesPF>() : make_lines<N, true, false, kLinesPF>();
+  if (asm_mode == 1)
+    return massb ? make_lines<N, false, true, kLinesPF, M, 0, true, true, 1>()
+                 : make_lines<N, false, false, kLinesPF, M, 0, true, true, 1>();
+  if (asm_mode == 2) return make_lines<N, false, false, kLinesPF, M, 0, true, true, 2>();  // mass mode 0 only
   return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
 }
 
-// experiment hook: HB_AX_VARIANT selects tuning variants of the N=7 plain kernel
 #ifdef HB_TUNE
 // Tuning build (-DHB_TUNE): per-N launch-shape variants selected with HB_AX_VN / HB_AX_VARIANT.
 template <int N, int EPBX, int REGS>
@@ -159,30 +163,30 @@ AxKernel pick_ax_variant(int N, int v) {
 }
 #endif
 
-AxKernel pick_ax(int N, bool halo, bool massb) {
+AxKernel pick_ax(int N, bool halo, bool massb, int asm_mode = 0) {
 #ifdef HB_TUNE
-  if (!halo && !massb) {
+  if (!halo && !massb && asm_mode == 0) {
     const char* v = getenv("HB_AX_VARIANT");
     const char* vn = getenv("HB_AX_VN");
     if (v && atoi(v) > 0 && vn && atoi(vn) == N) return pick_ax_variant(N, atoi(v));
   }
 #endif
   switch (N) {
-    case 1: return pick_ax_n<1>(halo, massb);
-    case 2: return pick_ax_n<2>(halo, massb);
-    case 3: return pick_ax_n<3>(halo, massb);
-    case 4: return pick_ax_n<4>(halo, massb);
-    case 5: return pick_ax_n<5>(halo, massb);
-    case 6: return pick_ax_n<6>(halo, massb);
-    case 7: return pick_ax_n<7>(halo, massb);
-    case 8: return pick_ax_n<8>(halo, massb);
-    case 9: return pick_ax_n<9>(halo, massb);
-    case 10: return pick_ax_n<10>(halo, massb);
-    case 11: return pick_ax_n<11>(halo, massb);
-    case 12: return pick_ax_n<12>(halo, massb);
-    case 13: return pick_ax_n<13>(halo, massb);
-    case 14: return pick_ax_n<14>(halo, massb);
-    default: return pick_ax_n<15>(halo, massb);
+    case 1: return pick_ax_n<1>(halo, massb, asm_mode);
+    case 2: return pick_ax_n<2>(halo, massb, asm_mode);
+    case 3: return pick_ax_n<3>(halo, massb, asm_mode);
+    case 4: return pick_ax_n<4>(halo, massb, asm_mode);
+    case 5: return pick_ax_n<5>(halo, massb, asm_mode);
+    case 6: return pick_ax_n<6>(halo, massb, asm_mode);
+    case 7: return pick_ax_n<7>(halo, massb, asm_mode);
+    case 8: return pick_ax_n<8>(halo, massb, asm_mode);
+    case 9: return pick_ax_n<9>(halo, massb, asm_mode);
+    case 10: return pick_ax_n<10>(halo, massb, asm_mode);
+    case 11: return pick_ax_n<11>(halo, massb, asm_mode);
+    case 12: return pick_ax_n<12>(halo, massb, asm_mode);
+    case 13: return pick_ax_n<13>(halo, massb, asm_mode);
+    case 14: return pick_ax_n<14>(halo, massb, asm_mode);
+    default: return pick_ax_n<15>(halo, massb, asm_mode);
   }
 }
 
@@ -248,6 +252,9 @@ struct hb_op {
   bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
   int variant = 0;      // 0: fused scatter-add (fp64 RED); 1: y_L + CSR gather (deterministic), P = 1
   DevBuf yL, csr_ptr, csr_slots;
+  // NekBone scattered storage (NEXT #4): local vectors of length N_L and the weights W
+  bool scat_mode = false;  // operator launches read x_L (sL_p) and write y_L
+  DevBuf sL_x, sL_r, sL_p, sL_w, sW;
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
   bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
@@ -255,7 +262,7 @@ struct hb_op {
   std::vector<int64_t> soff, scnt, roff, rcnt;
   int64_t n_send = 0;
   int last_grid = 0;  // grid of the last operator launch (number of energy partials, P = 1)
-  AxKernel ax_plain, ax_halo;
+  AxKernel ax_plain, ax_halo, ax_yl, ax_scat;  // ax_yl / ax_scat picked on first use
   cudaStream_t comm_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture (the legacy stream cannot be captured)
   cudaStream_t cap_stream2 = nullptr; // captures the body of the tolerance-mode WHILE node
@@ -288,6 +295,7 @@ struct hb_op {
     bool operator<(const TolKey& o) const { return std::tie(K, b, x, eps, st) < std::tie(o.K, o.b, o.x, o.eps, o.st); }
   };
   std::map<TolKey, GraphVal> tol_graphs;  // tolerance mode, one CUDA graph with a WHILE node
+  std::map<std::tuple<int32_t, const double*, double*>, GraphVal> scat_graphs;  // scattered-storage CG
   double* host_scal = nullptr;  // pinned CgScalars mirror
   ~hb_op() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -298,6 +306,7 @@ struct hb_op {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_stream2) cudaStreamDestroy(cap_stream2);
     for (auto& kv : tol_graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : scat_graphs) cudaGraphExecDestroy(kv.second.exec);
     if (ev_cap) cudaEventDestroy(ev_cap);
     for (cudaEvent_t e : {ev_pack, ev_halo, ev_haloel, ev_gather, ev_red, ev_red_done}) if (e) cudaEventDestroy(e);
     if (host_scal) cudaFreeHost(host_scal);
@@ -315,6 +324,15 @@ cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
                                              : cudaEventRecord(ev, st);
 }
 
+// dynamic shared memory opt-in and the persistent grid size (resident CTAs x SMs)
+int prepare_kernel(AxKernel& k) {
+  int nb = 0;
+  CU_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+  CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k.fn, k.block, k.smem));
+  k.grid_max = std::max(1, nb) * num_sms();
+  return HB_OK;
+}
+
 int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double* x, double* y, cudaStream_t st,
               bool energy = false, bool final_launch = false) {
   if (e1 <= e0) return HB_OK;
@@ -326,7 +344,8 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.xh = op->xh.as<double>();
   a.y = y;
   a.yh = op->yh.as<double>();
-  a.yL = op->variant == 1 ? op->yL.as<double>() : nullptr;
+  if (op->variant == 1 || op->scat_mode) a.yh = op->yL.as<double>();  // ASM >= 1 kernels write y_L there
+  if (op->scat_mode) a.xh = op->sL_p.as<double>();                     // ASM == 2 reads x_L there
   a.e_begin = e0; a.e_end = e1;
   a.n_owned = (int32_t)op->sz.n_owned;
   a.lam = op->lam;
@@ -354,19 +373,7 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
     op->prof_used++;
     CU_TRY(record_event(e_start, st));
   }
-  if (op->pdl && energy) {
-    // CG iteration (P = 1): programmatic dependent launch -- the operator grid is scheduled
-    // while the previous vector update drains and waits in-kernel (griddepcontrol.wait)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid); cfg.blockDim = dim3(k.block); cfg.dynamicSmemBytes = k.smem; cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at; cfg.numAttrs = 1;
-    CU_TRY(cudaLaunchKernelExC(&cfg, k.fn, args));
-  } else {
-    CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
-  }
+  CU_TRY(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.block), args, k.smem, st));
   op->launches++;
   if (timed) CU_TRY(record_event(e_stop, st));
   return HB_OK;
@@ -493,7 +500,7 @@ int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStrea
   const bool multi = op->comm && op->comm->P > 1;
   if (!multi) {
     if (op->variant == 1) {  // y_L, then the deterministic CSR gather (adds lambda x in mode 0)
-      HB_TRY(launch_ax(op, op->ax_plain, 0, E, x, y, st, energy, true));
+      HB_TRY(launch_ax(op, op->ax_yl, 0, E, x, y, st, energy, true));
       const int64_t n = op->sz.n_owned;
       hbk::csr_gather_kernel<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
           op->csr_ptr.as<int32_t>(), op->csr_slots.as<int32_t>(), op->yL.as<double>(), x,
@@ -654,13 +661,8 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
   // kernels
   op->ax_plain = pick_ax(N, false, op->mass_mode == 1);
   op->ax_halo = pick_ax(N, true, op->mass_mode == 1);
-  for (AxKernel* k : {&op->ax_plain, &op->ax_halo}) {
-    int nb = 0;
-    CU_TRY(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
-    CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k->fn, k->block, k->smem));
-    k->grid_max = std::max(1, nb) * num_sms();
-  }
-  HB_TRY(op->e_part.alloc((size_t)std::max(op->ax_plain.grid_max, op->ax_halo.grid_max) * 8 + 64));
+  for (AxKernel* k : {&op->ax_plain, &op->ax_halo}) HB_TRY(prepare_kernel(*k));
+  HB_TRY(op->e_part.alloc((size_t)std::max({op->ax_plain.grid_max, op->ax_halo.grid_max, 32 * num_sms()}) * 8 + 64));
   // P = 1: fused cooperative vector update (grid barrier instead of a second kernel)
   if (m->P == 1 && !comm) {
     int dev = 0, coop = 0, nb = 0;
@@ -858,6 +860,8 @@ int ensure_hist(hb_op* op, int32_t K) {
     op->graphs.clear();
     for (auto& kv : op->tol_graphs) cudaGraphExecDestroy(kv.second.exec);
     op->tol_graphs.clear();
+    for (auto& kv : op->scat_graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->scat_graphs.clear();
     HB_TRY(op->hist.alloc(need));
   }
   return HB_OK;
@@ -1051,6 +1055,26 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
   return HB_OK;
 }
 
+// CSR of Z^T over owned DOFs, slots in ascending (e, n) order (counting sort by gid), and the
+// y_L buffer -- shared by the deterministic variant and the scattered-storage CG
+static int ensure_csr(hb_op* op) {
+  if (op->yL.p) return HB_OK;
+  const int64_t n = op->sz.n_owned, NL = op->sz.N_L;
+  std::vector<int32_t> idx(NL);
+  CU_TRY(cudaMemcpy(idx.data(), op->idx.p, NL * 4, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> ptr(n + 1, 0), slots(NL);
+  for (int64_t t = 0; t < NL; ++t) ptr[idx[t] + 1]++;
+  for (int64_t g = 0; g < n; ++g) ptr[g + 1] += ptr[g];
+  std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+  for (int64_t t = 0; t < NL; ++t) slots[fill[idx[t]]++] = (int32_t)t;
+  HB_TRY(op->csr_ptr.alloc((n + 1) * 4));
+  HB_TRY(op->csr_slots.alloc(NL * 4));
+  HB_TRY(op->yL.alloc(NL * 8));
+  CU_TRY(cudaMemcpy(op->csr_ptr.p, ptr.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+  CU_TRY(cudaMemcpy(op->csr_slots.p, slots.data(), NL * 4, cudaMemcpyHostToDevice));
+  return HB_OK;
+}
+
 extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
   if (!op || variant < 0 || variant > 1) { set_error("hb_op_set_variant: bad argument"); return HB_ERR_ARG; }
   if (variant == 1 && (op->sz.P > 1 || op->comm)) {
@@ -1058,21 +1082,12 @@ extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
     return HB_ERR_STATE;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (variant == 1 && !op->yL.p) {
-    // CSR of Z^T over owned DOFs, slots in ascending (e, n) order (counting sort by gid)
-    const int64_t n = op->sz.n_owned, NL = op->sz.N_L;
-    std::vector<int32_t> idx(NL);
-    CU_TRY(cudaMemcpy(idx.data(), op->idx.p, NL * 4, cudaMemcpyDeviceToHost));
-    std::vector<int32_t> ptr(n + 1, 0), slots(NL);
-    for (int64_t t = 0; t < NL; ++t) ptr[idx[t] + 1]++;
-    for (int64_t g = 0; g < n; ++g) ptr[g + 1] += ptr[g];
-    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
-    for (int64_t t = 0; t < NL; ++t) slots[fill[idx[t]]++] = (int32_t)t;
-    HB_TRY(op->csr_ptr.alloc((n + 1) * 4));
-    HB_TRY(op->csr_slots.alloc(NL * 4));
-    HB_TRY(op->yL.alloc(NL * 8));
-    CU_TRY(cudaMemcpy(op->csr_ptr.p, ptr.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
-    CU_TRY(cudaMemcpy(op->csr_slots.p, slots.data(), NL * 4, cudaMemcpyHostToDevice));
+  if (variant == 1) {
+    HB_TRY(ensure_csr(op));
+    if (!op->ax_yl.fn) {
+      op->ax_yl = pick_ax(op->N, false, op->mass_mode == 1, 1);
+      HB_TRY(prepare_kernel(op->ax_yl));
+    }
   }
   (void)st;
   if (variant != op->variant) {
@@ -1083,6 +1098,124 @@ extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
   }
   op->variant = variant;
   return HB_OK;
+}
+
+// ---------------------------------------------------------------- scattered storage CG
+namespace {
+int scat_setup(hb_op* op) {
+  HB_TRY(ensure_csr(op));
+  if (!op->ax_scat.fn) {
+    op->ax_scat = pick_ax(op->N, false, false, 2);
+    HB_TRY(prepare_kernel(op->ax_scat));
+  }
+  if (op->sW.p) return HB_OK;
+  const int64_t NL = op->sz.N_L;
+  for (DevBuf* b : {&op->sL_x, &op->sL_r, &op->sL_p, &op->sL_w, &op->sW}) HB_TRY(b->alloc(NL * 8));
+  // W_s = 1 / (number of slots of the slot's DOF): from the CSR row lengths
+  const int64_t n = op->sz.n_owned;
+  std::vector<int32_t> ptr(n + 1), idx(NL);
+  CU_TRY(cudaMemcpy(ptr.data(), op->csr_ptr.p, (n + 1) * 4, cudaMemcpyDeviceToHost));
+  CU_TRY(cudaMemcpy(idx.data(), op->idx.p, NL * 4, cudaMemcpyDeviceToHost));
+  std::vector<double> W(NL);
+  for (int64_t t = 0; t < NL; ++t) W[t] = 1.0 / (double)(ptr[idx[t] + 1] - ptr[idx[t]]);
+  CU_TRY(cudaMemcpy(op->sW.p, W.data(), NL * 8, cudaMemcpyHostToDevice));
+  return HB_OK;
+}
+
+int scat_iteration(hb_op* op, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned, NL = op->sz.N_L;
+  hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
+  const int gl = vec_grid(2 * NL);
+  op->scat_mode = true;
+  const int stt = launch_ax(op, op->ax_scat, 0, op->sz.E_local, nullptr, nullptr, st);  // y_L = S_L p_L
+  op->scat_mode = false;
+  HB_TRY(stt);
+  hbk::gs_scatter_kernel<<<vec_grid(2 * n), hbk::VEC_BLOCK, 0, st>>>(op->csr_ptr.as<int32_t>(), op->csr_slots.as<int32_t>(),
+                                                                   op->yL.as<double>(), op->sL_p.as<double>(), op->lam,
+                                                                   op->sL_w.as<double>(), n);
+  hbk::wdot_kernel<<<gl, hbk::VEC_BLOCK, 0, st>>>(op->sW.as<double>(), op->sL_p.as<double>(), op->sL_w.as<double>(), NL,
+                                                  op->partials.as<double>(), &s->ticket, &s->pAp);
+  hbk::scat_update_xr<<<gl, hbk::VEC_BLOCK, 0, st>>>(op->sL_x.as<double>(), op->sL_p.as<double>(), op->sL_r.as<double>(),
+                                                     op->sL_w.as<double>(), op->sW.as<double>(), NL,
+                                                     op->partials.as<double>(), s, op->hist.as<double>());
+  hbk::scat_update_p<<<gl, hbk::VEC_BLOCK, 0, st>>>(op->sL_p.as<double>(), op->sL_r.as<double>(), NL, s);
+  op->launches += 4;
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+int scat_init(hb_op* op, const double* b, cudaStream_t st) {
+  const int64_t NL = op->sz.N_L;
+  hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
+  const int gl = vec_grid(2 * NL);
+  hbk::scatter_kernel<<<gl, hbk::VEC_BLOCK, 0, st>>>(op->idx.as<int32_t>(), b, op->sL_r.as<double>(), NL);
+  CU_TRY(cudaMemcpyAsync(op->sL_p.p, op->sL_r.p, NL * 8, cudaMemcpyDeviceToDevice, st));
+  CU_TRY(cudaMemsetAsync(op->sL_x.p, 0, NL * 8, st));
+  CU_TRY(cudaMemsetAsync(&s->it, 0, sizeof(int32_t), st));
+  hbk::wdot_kernel<<<gl, hbk::VEC_BLOCK, 0, st>>>(op->sW.as<double>(), op->sL_r.as<double>(), op->sL_r.as<double>(), NL,
+                                                  op->partials.as<double>(), &s->ticket, &s->rr_new);
+  op->launches += 2;
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+}  // namespace
+
+extern "C" int hb_cg_solve_scattered(hb_op* op, const double* b, double* x, int32_t max_iters, double eps,
+                                     double* rr_hist_host, hb_cg_result* res, void* stream) {
+  if (!op || (op->sz.n_owned > 0 && (!b || !x)) || max_iters < 0) { set_error("hb_cg_solve_scattered: bad argument"); return HB_ERR_ARG; }
+  if (op->sz.P > 1 || op->comm || op->mass_mode != 0) {
+    set_error("hb_cg_solve_scattered: NekBone's scattered storage is implemented for P = 1, mass mode 0");
+    return HB_ERR_STATE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  HB_TRY(scat_setup(op));
+  HB_TRY(ensure_hist(op, max_iters));
+  int32_t iters = 0;
+  if (eps < 0) {  // fixed mode: one captured graph per (K, b, x), like hb_cg_solve
+    auto key = std::make_tuple(max_iters, b, x);
+    auto it = op->scat_graphs.find(key);
+    if (it == op->scat_graphs.end()) {
+      const int64_t l0 = op->launches;
+      cudaStream_t cs = op->cap_stream;
+      cudaGraph_t graph;
+      CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int status = scat_init(op, b, cs);
+      for (int32_t j = 0; j < max_iters && status == HB_OK; ++j) status = scat_iteration(op, cs);
+      cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+      if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
+      CU_TRY(ce);
+      cudaGraphExec_t exec;
+      cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CU_TRY(ie);
+      it = op->scat_graphs.emplace(key, hb_op::GraphVal{exec, op->launches - l0, 0, 0, 0}).first;
+      op->launches = l0;
+    }
+    CU_TRY(cudaGraphLaunch(it->second.exec, st));
+    op->launches += it->second.launches;
+    iters = max_iters;
+  } else {
+    HB_TRY(scat_init(op, b, st));
+    hbk::CgScalars* hs = reinterpret_cast<hbk::CgScalars*>(op->host_scal);
+    CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    while (iters < max_iters && hs->rr_new > eps) {
+      HB_TRY(scat_iteration(op, st));
+      CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+      CU_TRY(cudaStreamSynchronize(st));
+      if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp)) {
+        set_error("hb_cg_solve_scattered: breakdown at iteration " + std::to_string(iters));
+        return HB_ERR_BREAKDOWN;
+      }
+      ++iters;
+    }
+  }
+  const int64_t n = op->sz.n_owned;
+  hbk::pick_kernel<<<vec_grid(2 * n), hbk::VEC_BLOCK, 0, st>>>(op->csr_ptr.as<int32_t>(), op->csr_slots.as<int32_t>(),
+                                                             op->sL_x.as<double>(), x, n);
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  return finish_result(op, iters, rr_hist_host, res, st);
 }
 
 extern "C" int hb_op_set_jacobi(hb_op* op, int enable, void* stream) {

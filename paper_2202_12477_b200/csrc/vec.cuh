@@ -394,6 +394,84 @@ csr_gather_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict
   }
 }
 
+// ---- NekBone's scattered storage: vectors of length N_L
+// (x_L = Z x_G), the operator (Z Z^T S_L + lambda I) x_L with a combined gather-scatter, and
+// inner products weighted by the inverse counting vector W.
+
+// w_L = Z Z^T yL + lambda p_L: one thread per global DOF sums its slots (CSR, ascending (e,n))
+// and writes the sum to every slot.
+__global__ void __launch_bounds__(VEC_BLOCK)
+gs_scatter_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ slots,
+                  const double* __restrict__ yL, const double* __restrict__ pL, double lam, double* __restrict__ wL,
+                  int64_t n) {
+  for (int64_t g = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; g < n; g += (int64_t)gridDim.x * VEC_BLOCK) {
+    const int32_t t0 = row_ptr[g], t1 = row_ptr[g + 1];
+    double acc = 0.0;
+    for (int32_t t = t0; t < t1; ++t) acc += yL[slots[t]];
+    for (int32_t t = t0; t < t1; ++t) {
+      const int32_t sl = slots[t];
+      wL[sl] = fma(lam, pL[sl], acc);
+    }
+  }
+}
+
+// W-weighted dot sum_s W_s a_s b_s -> *out (allreduce-free, P = 1)
+__global__ void __launch_bounds__(VEC_BLOCK)
+wdot_kernel(const double* __restrict__ W, const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+            double* partials, uint32_t* ticket, double* out) {
+  double acc = 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK)
+    acc = fma(W[l] * a[l], b[l], acc);
+  double tot;
+  if (finish_reduction(acc, partials, ticket, &tot)) *out = tot;
+}
+
+// alpha = rr / pAp; x += alpha p; r -= alpha w; W-weighted r.r -> rr_new (scattered CG)
+__global__ void __launch_bounds__(VEC_BLOCK)
+scat_update_xr(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
+               const double* __restrict__ w, const double* __restrict__ W, int64_t n, double* partials, CgScalars* s,
+               double* hist) {
+  const double rr = s->rr_new;
+  const double pAp = s->pAp;
+  const double alpha = (pAp != 0.0) ? rr / pAp : 0.0;
+  double acc = 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK) {
+    x[l] = fma(alpha, p[l], x[l]);
+    const double rv = fma(-alpha, w[l], r[l]);
+    r[l] = rv;
+    acc = fma(W[l] * rv, rv, acc);
+  }
+  double tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) {
+    s->rr = rr;
+    if (hist) hist[s->it] = rr;
+    s->rr_new = tot;
+  }
+}
+
+// beta = rr_new / rr; p = r + beta p (scattered CG)
+__global__ void __launch_bounds__(VEC_BLOCK)
+scat_update_p(double* __restrict__ p, const double* __restrict__ r, int64_t n, CgScalars* s) {
+  const double rr = s->rr;
+  const double beta = (rr != 0.0) ? s->rr_new / rr : 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n; l += (int64_t)gridDim.x * VEC_BLOCK)
+    p[l] = fma(beta, p[l], r[l]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s->it += 1;
+}
+
+// x_L = Z x_G (scatter) and x_G = one slot of each DOF (gather back of a scattered vector)
+__global__ void __launch_bounds__(VEC_BLOCK)
+scatter_kernel(const int32_t* __restrict__ idx, const double* __restrict__ xg, double* __restrict__ xl, int64_t nl) {
+  for (int64_t s = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; s < nl; s += (int64_t)gridDim.x * VEC_BLOCK)
+    xl[s] = xg[idx[s]];
+}
+__global__ void __launch_bounds__(VEC_BLOCK)
+pick_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ slots, const double* __restrict__ xl,
+            double* __restrict__ xg, int64_t n) {
+  for (int64_t g = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; g < n; g += (int64_t)gridDim.x * VEC_BLOCK)
+    xg[g] = xl[slots[row_ptr[g]]];
+}
+
 // Jacobi preconditioner (NekBone's "simple diagonal preconditioning",
 // P:140): diag(A)_g = sum over the slots of g of (S_L^e)_nn (+ lambda B_n in mass mode 1);
 // (S_L^e)_nn = sum_m D[m][i]^2 Grr(m,j,k) + D[m][j]^2 Gss(i,m,k) + D[m][k]^2 Gtt(i,j,m)

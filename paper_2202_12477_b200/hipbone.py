@@ -82,6 +82,7 @@ _SIGS = {
     "hb_forcing": (C.c_int, [_p, C.c_uint64, _p, _p]),
     "hb_dot": (C.c_int, [_p, _p, _p, _dp, _p]),
     "hb_cg_solve": (C.c_int, [_p, _p, _p, C.c_int32, C.c_double, _dp, C.POINTER(hb_cg_result), _p]),
+    "hb_cg_solve_scattered": (C.c_int, [_p, _p, _p, C.c_int32, C.c_double, _dp, C.POINTER(hb_cg_result), _p]),
     "hb_cg_solve_host": (C.c_int, [_p, _dp, _dp, C.c_int32, C.c_double, _dp, C.POINTER(hb_cg_result), _p]),
     "hb_op_set_profiling": (C.c_int, [_p, C.c_int]),
     "hb_op_set_jacobi": (C.c_int, [_p, C.c_int, _p]),
@@ -290,6 +291,14 @@ class Operator:
         res = hb_cg_result()
         _check(_lib.hb_cg_solve(self._h, _dev(b), _dev(x), max_iters, eps, _ptr(hist, C.c_double),
                                 C.byref(res), _stream(stream)))
+        return res.iterations, hist[:res.iterations + 1].copy()
+
+    def cg_scattered(self, b, x, max_iters: int, eps: float = -1.0, stream=None):
+        """NekBone's scattered-storage CG (P = 1, mass mode 0); same return as cg()."""
+        hist = np.zeros(max_iters + 1)
+        res = hb_cg_result()
+        _check(_lib.hb_cg_solve_scattered(self._h, _dev(b), _dev(x), max_iters, eps, _ptr(hist, C.c_double),
+                                          C.byref(res), _stream(stream)))
         return res.iterations, hist[:res.iterations + 1].copy()
 
     def cg_host(self, b: np.ndarray, x: np.ndarray, max_iters: int, eps: float = -1.0, stream=None,

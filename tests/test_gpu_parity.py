@@ -491,3 +491,30 @@ def test_deterministic_csr_variant(hb, N, mass_mode):
     xo, jo, ho = ocg.cg(lambda v: o.apply(v, 1.0), bo, max_iters=30)
     jt = min(30, next((k for k, v in enumerate(ho) if v <= 1e-16 * ho[0]), 30))
     _cg_contract(h1, ho, jt - 1)
+
+
+@pytest.mark.parametrize("box,N", [((2, 2, 2), 3), ((5, 4, 3), 7)])
+def test_scattered_storage_cg(hb, box, N):
+    """NekBone's scattered storage (NEXT #4): CG on x_L = Z x with Z Z^T S_L +
+    lambda I and W-weighted dots has the same iterates as the assembled CG (the weighted
+    dots equal the assembled ones), so it must match the oracle's Alg. 1 (c18)."""
+    o = OracleProblem(box, N)
+    A = lambda v: o.apply(v, 1.0)
+    bo = of.forcing(range(o.NG), 1)
+    eps = 1e-16 * ocg.dot(bo, bo)
+    xo, jo, ho = ocg.cg(A, bo, max_iters=200, eps=eps)
+    m = hb.Mesh(*box, N)
+    op = hb.Operator(m)
+    b = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.forcing(1, b)
+    x = torch.zeros_like(b)
+    j, h = op.cg_scattered(b, x, 200, eps)
+    assert j == jo
+    _cg_contract(h, ho, jo - 1)
+    assert np.abs(x.cpu().numpy() - xo).max() <= 1e-10 * np.abs(xo).max()
+    x = torch.zeros_like(b)
+    jf, hf = op.cg_scattered(b, x, jo)  # fixed mode, captured graph
+    assert jf == jo
+    _cg_contract(hf, ho, jo - 1)
+    with pytest.raises(hb.HBError, match="STATE"):
+        hb.Operator(hb.Mesh(*box, N, mass_mode=1)).cg_scattered(b, x, 3)
