@@ -74,6 +74,8 @@ struct LinesShape {
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
+  // per-element L2 prefetch of G: a gain from N = 6 up, a 1-3% loss below (profiles/r1_tune2.jsonl)
+  static constexpr bool PFL_DEF = N >= 6;
 };
 
 // sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs
@@ -200,8 +202,9 @@ __device__ __forceinline__ double ldG(const double* p) {
 
 // ASM: 0 = fused scatter-add into assembled storage (fp64 RED / store); 1 = write y_L per slot
 // (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L.
-template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0, bool PFL = true,
-          bool GCS = true, int ASM = 0>
+template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0,
+          bool PFL = LinesShape<N>::PFL_DEF,
+          bool GCS = true, int ASM = 0, bool PFN = false>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
@@ -251,8 +254,17 @@ ax_lines(const AxArgs a) {
     // gather and two barriers) and of the next element's index block (next P1).
     if constexpr (PFL) {
       if (act) {
-        const char* gb = reinterpret_cast<const char*>(a.G + e * (6 * NP3));
-        for (int q = t - le * NP2; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(gb + q * 128);
+        // PFN: fetch the NEXT element's G one whole element ahead (the first element at the
+        // first iteration); otherwise this element's G at the start of its gather
+        const int64_t eg = PFN ? e + (int64_t)gridDim.x * EPB : e;
+        if (PFN && base == a.e_begin + (int64_t)blockIdx.x * EPB) {
+          const char* g0 = reinterpret_cast<const char*>(a.G + e * (6 * NP3));
+          for (int q = t - le * NP2; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(g0 + q * 128);
+        }
+        if (eg < a.e_end) {
+          const char* gb = reinterpret_cast<const char*>(a.G + eg * (6 * NP3));
+          for (int q = t - le * NP2; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(gb + q * 128);
+        }
         const int64_t en = e + (int64_t)gridDim.x * EPB;
         if (en < a.e_end) {
           const char* ib = reinterpret_cast<const char*>(a.idx + en * NP3);

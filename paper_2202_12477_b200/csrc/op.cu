@@ -90,11 +90,11 @@ struct AxKernel {
   size_t smem = 0;
 };
 
-template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0, bool PFL = true,
-          bool GCS = true, int ASM = 0>
+template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0,
+          bool PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
@@ -107,10 +107,11 @@ template <int N>
 AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
   constexpr int M = hbk::LinesShape<N>::MINB;
   if (halo) return massb ? make_lines<N, true, true, kLinesPF>() : make_lines<N, true, false, kLinesPF>();
+  constexpr bool PL = hbk::LinesShape<N>::PFL_DEF;
   if (asm_mode == 1)
-    return massb ? make_lines<N, false, true, kLinesPF, M, 0, true, true, 1>()
-                 : make_lines<N, false, false, kLinesPF, M, 0, true, true, 1>();
-  if (asm_mode == 2) return make_lines<N, false, false, kLinesPF, M, 0, true, true, 2>();  // mass mode 0 only
+    return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 1>()
+                 : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 1>();
+  if (asm_mode == 2) return make_lines<N, false, false, kLinesPF, M, 0, PL, true, 2>();  // mass mode 0 only
   return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
 }
 
@@ -138,6 +139,8 @@ AxKernel tune_variant(int v) {
     case 4: return make_lines<N, false, false, 0, 1>();
     case 5: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>()>();
     case 6: return make_lines<N, false, false, 0, tune_minb<N, E128, 128>(), E128>();
+    case 7: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, true, true, 0, true>();  // G one element ahead
+    case 8: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, false>();                // no G prefetch
     default: return make_lines<N, false, false, kLinesPF>();
   }
 }
