@@ -68,7 +68,11 @@ struct LinesShape {
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
   // Resident CTAs per SM requested from ptxas, from a per-N register target measured on the
   // B200 (profiles/r1_tune.jsonl; 0 = no cap, one CTA per SM), capped by shared memory.
-  static constexpr int REGS_T[16] = {0, 64, 64, 64, 96, 96, 128, 128, 128, 128, 128, 128, 0, 128, 0, 0};
+  // N = 12: streaming line contractions (no output arrays) fit 2 CTAs/SM without spills
+  // (0.69 vs 0.57 of peak); for N = 13..15 the streamed kernel at 2 CTAs/SM spills and loses
+  // to one uncapped CTA per SM (profiles/r1_opbench_sweep.jsonl, r1_tune.jsonl)
+  static constexpr bool STREAM = N == 12;
+  static constexpr int REGS_T[16] = {0, 64, 64, 64, 96, 96, 128, 128, 128, 128, 128, 128, 160, 128, 0, 0};
   static constexpr int REGS = REGS_T[N];
   static constexpr int MINB_REG0 = REGS ? 65536 / (BLOCK * REGS) : 1;
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
@@ -202,6 +206,38 @@ __device__ __forceinline__ double ldG(const double* p) {
 
 // ASM: 0 = fused scatter-add into assembled storage (fp64 RED / store); 1 = write y_L per slot
 // (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L.
+// Streaming form of eo_apply for one line: each output y_i is handed to sink(i, y_i) as soon
+// as it is formed (the input line is folded into e/o first, so it may be overwritten in place);
+// no output array is kept -- large N stays within the register budget of 2 CTAs per SM.
+template <int N, int EPBX, class Sink>
+__device__ __forceinline__ void eo_apply_sink(const double* __restrict__ sM, const double (&x)[N + 1], Sink&& sink) {
+  using S = LinesShape<N, EPBX>;
+  constexpr int H = S::H, HE = S::HE, ODD = S::ODD, HE2 = S::HE2, H2 = S::H2;
+  const double* Me = sM;
+  const double* Mo = sM + H * HE2;
+  const double* Mm = Mo + H * H2;
+  double e[1][HE], o[1][H > 0 ? H : 1];
+#pragma unroll
+  for (int m = 0; m < H; ++m) {
+    e[0][m] = x[m] + x[N - m];
+    o[0][m] = x[m] - x[N - m];
+  }
+  if constexpr (ODD) e[0][H] = x[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double se[1] = {0.0}, so[1] = {0.0};
+    dot_rows<HE, 1, HE>(Me + i * HE2, e, se);
+    dot_rows<H, 1, (H > 0 ? H : 1)>(Mo + i * H2, o, so);
+    sink(i, so[0] + se[0]);
+    sink(N - i, so[0] - se[0]);
+  }
+  if constexpr (ODD) {
+    double sm[1] = {0.0};
+    dot_rows<H, 1, (H > 0 ? H : 1)>(Mm, o, sm);
+    sink(H, sm[0]);
+  }
+}
+
 template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0,
           bool PFL = LinesShape<N>::PFL_DEF,
           bool GCS = true, int ASM = 0, bool PFN = false>
@@ -291,7 +327,15 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
-    {
+    if constexpr (S::STREAM) {
+      double in[NP];
+#pragma unroll
+      for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(m, ca, cb)];
+      eo_apply_sink<N, EPBX>(s_D, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+#pragma unroll
+      for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(ca, m, cb)];
+      eo_apply_sink<N, EPBX>(s_D, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
+    } else {
       double in[2][NP], out[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
@@ -330,7 +374,15 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
-    {
+    if constexpr (S::STREAM) {
+      double in[NP];
+#pragma unroll
+      for (int m = 0; m < NP; ++m) in[m] = s_r[S::at(m, ca, cb)];
+      eo_apply_sink<N, EPBX>(s_DT, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+#pragma unroll
+      for (int m = 0; m < NP; ++m) in[m] = s_s[S::at(ca, m, cb)];
+      eo_apply_sink<N, EPBX>(s_DT, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
+    } else {
       double in[2][NP], out[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
@@ -348,12 +400,10 @@ ax_lines(const AxArgs a) {
 
     // ---- P5: t-direction transposed contraction, sum, assembly Z^T
     if (act) {
-      double vt[1][NP];
-      eo_apply<N, EPBX, 1>(s_DT, gt, vt);
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
+      // node k of the (i,j) column: sum the three directions, lambda terms, assembly Z^T
+      auto node = [&](int k, double vtk) {
         const int o = S::at(ca, cb, k);
-        double out = vt[0][k] + s_r[o] + s_s[o];
+        double out = vtk + s_r[o] + s_s[o];
         const double uk = s_u[o];
         en = fma(uk, out, en);
         if (MASSB) {
@@ -369,6 +419,14 @@ ax_lines(const AxArgs a) {
         } else {
           red_y<HALO>(a, gi[k], out);
         }
+      };
+      if constexpr (S::STREAM) {
+        eo_apply_sink<N, EPBX>(s_DT, gt[0], node);
+      } else {
+        double vt[1][NP];
+        eo_apply<N, EPBX, 1>(s_DT, gt, vt);
+#pragma unroll
+        for (int k = 0; k < NP; ++k) node(k, vt[0][k]);
       }
     }
     __syncthreads();
