@@ -339,6 +339,10 @@ def main():
                           "storage": args.storage},
                "gdofs_per_s": round(gdofs, 4),
                "cg_bytes_per_iter_fused": ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3),
+               # bytes per DOF per CG iteration: this build's algorithmic ledger vs the paper's
+               # assembled-storage minimum 108 + 80 N_L/N_G
+               "bytes_per_dof_iter": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) / NG, 2),
+               "bytes_per_dof_iter_paper": round(ledger.cg_bytes_paper(NG, E_glob * (N + 1) ** 3) / NG, 2),
                "cg_gbs_fused_ledger": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) * K / (ms * 1e-3) / 1e9, 1),
                "e2e": ({"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
                         "d2h_bytes_per_step": 8 * n + 48} if e2e_ms else None),
