@@ -132,6 +132,15 @@ int hb_mesh_destroy(hb_mesh* m);
 int hb_comm_unique_id(uint8_t id[128]);
 int hb_comm_create(int P, int rank, const uint8_t id[128], hb_comm** out);
 int hb_comm_destroy(hb_comm* c);
+/* Peer-memory transport (the direct-NVLink alternative to NCCL for the
+ * two exchanges of P:201-203 and the CG allreduces of P:213-217): no NCCL communicator; every
+ * op built on it must be connected with hb_op_ipc_connect before use.  Ranks on one node
+ * (any GPUs, or several ranks on one GPU).  Data moves with peer copies into the receiver's
+ * buffers (CUDA IPC mappings; NVLink copy engines across GPUs); ordering uses 32-bit sequence
+ * flags in the receiver's mailbox (stream memory operations), never a host synchronisation.
+ * Fixed-mode CG runs as a stream-ordered loop (no graph: the flags carry per-call sequence
+ * numbers).  HB_ERR_ARG on bad (P, rank). */
+int hb_comm_create_ipc(int P, int rank, hb_comm** out);
 
 /* ---------------------------------------------------------------- operator
  * hb_op_create uploads the local index, geometric factors (and B in mode 1) and exchange
@@ -142,6 +151,16 @@ int hb_op_create(const hb_mesh* m, hb_comm* comm, double lambda, void* stream, h
 /* y_dev = A x_dev on owned DOFs ([n_owned] each, distinct device buffers).  Fused
  * gather / S_L + lambda M_L / scatter-add kernel (P:154 extended by the Z^T fusion).  Asynchronous. */
 int hb_op_apply(hb_op* op, const double* x_dev, double* y_dev, void* stream);
+/* IPC transport bootstrap (op on an hb_comm_create_ipc communicator).  hb_op_ipc_blob_size
+ * gives the byte size B of this op's export record (same on every rank: a function of P);
+ * hb_op_ipc_export writes it (CUDA IPC handles of the mailbox, the halo receive buffer and
+ * the assembly receive buffer, plus the neighbour list, counts and offsets).  The caller
+ * all-gathers the P records (rank order, P*B bytes) and passes them to hb_op_ipc_connect,
+ * which maps every peer's mailbox and the buffers this rank writes into, and checks that the
+ * plans agree (HB_ERR_STATE otherwise).  Collective: every rank calls it once. */
+int hb_op_ipc_blob_size(const hb_op* op, int64_t* bytes);
+int hb_op_ipc_export(const hb_op* op, uint8_t* blob);
+int hb_op_ipc_connect(hb_op* op, const uint8_t* blobs);
 /* b_dev[l] = forcing(owned_gid[l], seed) (c12), [n_owned].  Asynchronous. */
 int hb_forcing(hb_op* op, uint64_t seed, double* b_dev, void* stream);
 /* global a.b over owned DOFs (allreduced for P>1); synchronises the stream. */

@@ -11,6 +11,7 @@
 // CG: per iteration  op(p) -> dot p.Ap [allreduce] -> x,r update + r.r [allreduce]
 // -> p update (writes the next assembly init lambda*p).  No host synchronisation inside the
 // loop; fixed-iteration mode is captured once into a CUDA graph and replayed.
+#include <cuda.h>  // driver types of the stream memory operations (entry points resolved at run time)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -58,6 +59,7 @@ using hb::set_error;
 struct hb_comm {
   ncclComm_t nccl = nullptr;
   int P = 1, rank = 0;
+  int kind = 0;  // 0: NCCL; 1: IPC peer-memory transport (hb_comm_create_ipc)
 };
 
 namespace {
@@ -300,7 +302,21 @@ struct hb_op {
   std::map<TolKey, GraphVal> tol_graphs;  // tolerance mode, one CUDA graph with a WHILE node
   std::map<std::tuple<int32_t, const double*, double*>, GraphVal> scat_graphs;  // scattered-storage CG
   double* host_scal = nullptr;  // pinned CgScalars mirror
+  // IPC transport (comm kind 1): peer mappings of the buffers this rank writes into
+  struct IpcPeer {
+    double* xh = nullptr;      // peer's halo receive buffer (+ xh_off: the segment from this rank)
+    double* recv = nullptr;    // peer's assembly receive buffer (+ recv_off)
+    uint32_t* flags = nullptr; // peer's mailbox flags [5][P]
+    double* vals = nullptr;    // peer's mailbox allreduce slots [2][P]
+    int64_t xh_off = 0, recv_off = 0;
+  };
+  bool ipc_ready = false;
+  DevBuf mbox, ipc_tab;  // mailbox; device tables of the P vals / AR-flag pointers
+  std::vector<IpcPeer> peers;
+  std::vector<void*> ipc_opened;
+  uint32_t apply_seq = 0, ar_seq = 0;
   ~hb_op() {
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto& pr : prof_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (Timer* tm : {&t_xr, &t_p})
@@ -400,8 +416,110 @@ int phase_event(hb_op* op, hb_op::Timer& tm, bool start, cudaStream_t st) {
   return HB_OK;
 }
 
+// --- IPC transport (comm kind 1).  Every rank maps, through CUDA IPC,
+// the mailbox of every peer and the halo / assembly receive buffers of its neighbours.  The
+// sender copies straight into the receiver's buffer (NVLink copy engine across GPUs) and then
+// raises a 32-bit sequence flag in the receiver's mailbox (cuStreamWriteValue32, fenced); the
+// receiver's stream waits on it (cuStreamWaitValue32 GEQ).  Per directed neighbour pair four
+// flags order one apply s:  HD (halo data in your xh, = s), HF (my xh is consumed, = s),
+// AD (assembly data in your recv, = s), AF (my recv is consumed, = s - 1, raised at the start
+// of the next apply).  Allreduce: every rank stores its value into slot [s & 1][me] of every
+// mailbox and raises AR = s; two slots suffice because no rank can start allreduce s + 2
+// before every rank has finished s (it needs their s + 1 values, pushed after their sum of s).
+// Mailbox layout: uint32 flags[5][P] (indexed by source rank), then double vals[2][P].
+enum { F_HD = 0, F_HF = 1, F_AD = 2, F_AF = 3, F_AR = 4, F_KINDS = 5 };
+size_t mbox_vals_off(int P) { return ((size_t)F_KINDS * P * 4 + 255) & ~size_t(255); }
+size_t mbox_bytes(int P) { return mbox_vals_off(P) + (size_t)2 * P * 8; }
+
+typedef CUresult (*PfnValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PfnValue32 g_wait32 = nullptr, g_write32 = nullptr;
+
+int load_memops() {
+  if (g_wait32 && g_write32) return HB_OK;
+  cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = cudaDriverEntryPointSymbolNotFound;
+  CU_TRY(cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", (void**)&g_wait32, 12000, cudaEnableDefault, &q1));
+  CU_TRY(cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", (void**)&g_write32, 12000, cudaEnableDefault, &q2));
+  if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !g_wait32 || !g_write32) {
+    g_wait32 = g_write32 = nullptr;
+    set_error("IPC transport: stream memory operations unavailable in this driver");
+    return HB_ERR_CUDA;
+  }
+  return HB_OK;
+}
+
+int mem_wait(cudaStream_t st, const uint32_t* addr, uint32_t v) {
+  CUresult r = g_wait32((CUstream)st, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) { set_error("cuStreamWaitValue32 failed (CUresult " + std::to_string((int)r) + ")"); return HB_ERR_CUDA; }
+  return HB_OK;
+}
+
+int mem_signal(cudaStream_t st, uint32_t* addr, uint32_t v) {
+  CUresult r = g_write32((CUstream)st, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);  // fenced
+  if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 failed (CUresult " + std::to_string((int)r) + ")"); return HB_ERR_CUDA; }
+  return HB_OK;
+}
+
+bool is_ipc(const hb_op* op) { return op->comm && op->comm->kind == 1; }
+
+// kind 0: halo exchange (owners push x at shared DOFs into the sharers' xh);
+// kind 1: assembly exchange (sharers push their halo partial sums yh into the owners' recv).
+int ipc_exchange(hb_op* op, int kind, cudaStream_t cs) {
+  const int P = op->comm->P, me = op->comm->rank;
+  uint32_t* own = op->mbox.as<uint32_t>();
+  auto own_flag = [&](int q, int k) { return own + k * P + q; };
+  auto peer_flag = [&](int q, int k) { return op->peers[q].flags + k * P + me; };
+  if (kind == 0) {
+    const uint32_t s = ++op->apply_seq;
+    for (size_t i = 0; i < op->nbr.size(); ++i) {
+      if (!op->scnt[i]) continue;
+      const int q = op->nbr[i];
+      HB_TRY(mem_signal(cs, peer_flag(q, F_AF), s - 1));  // the previous apply's recv from q is unpacked
+      HB_TRY(mem_wait(cs, own_flag(q, F_HF), s - 1));     // q has consumed the previous halo data
+      CU_TRY(cudaMemcpyAsync(op->peers[q].xh + op->peers[q].xh_off, op->send_buf.as<double>() + op->soff[i],
+                             op->scnt[i] * 8, cudaMemcpyDeviceToDevice, cs));
+      HB_TRY(mem_signal(cs, peer_flag(q, F_HD), s));
+    }
+    for (size_t i = 0; i < op->nbr.size(); ++i)
+      if (op->rcnt[i]) HB_TRY(mem_wait(cs, own_flag(op->nbr[i], F_HD), s));
+    return HB_OK;
+  }
+  const uint32_t s = op->apply_seq;
+  for (size_t i = 0; i < op->nbr.size(); ++i) {
+    if (!op->rcnt[i]) continue;
+    const int q = op->nbr[i];
+    HB_TRY(mem_signal(cs, peer_flag(q, F_HF), s));      // halo elements done: xh from q consumed
+    HB_TRY(mem_wait(cs, own_flag(q, F_AF), s - 1));     // q has unpacked the previous contribution
+    CU_TRY(cudaMemcpyAsync(op->peers[q].recv + op->peers[q].recv_off, op->yh.as<double>() + op->roff[i],
+                           op->rcnt[i] * 8, cudaMemcpyDeviceToDevice, cs));
+    HB_TRY(mem_signal(cs, peer_flag(q, F_AD), s));
+  }
+  for (size_t i = 0; i < op->nbr.size(); ++i)
+    if (op->scnt[i]) HB_TRY(mem_wait(cs, own_flag(op->nbr[i], F_AD), s));
+  return HB_OK;
+}
+
+int ipc_allreduce(hb_op* op, double* v, cudaStream_t st) {
+  const int P = op->comm->P, me = op->comm->rank;
+  const uint32_t s = ++op->ar_seq;
+  const int slot = (int)(s & 1);
+  double* const* vt = op->ipc_tab.as<double*>();
+  uint32_t* const* ft = reinterpret_cast<uint32_t* const*>(vt + P);
+  hbk::ipc_push_kernel<<<1, 32, 0, st>>>(v, vt, ft, P, me, slot, s);
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  uint32_t* own = op->mbox.as<uint32_t>();
+  for (int q = 0; q < P; ++q)
+    if (q != me) HB_TRY(mem_wait(st, own + F_AR * P + q, s));
+  double* vals = reinterpret_cast<double*>(op->mbox.as<char>() + mbox_vals_off(P));
+  hbk::ipc_sum_kernel<<<1, 1, 0, st>>>(vals + slot * P, P, v);
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
 int allreduce_sum(hb_op* op, double* v, cudaStream_t st) {
   if (!op->comm || op->comm->P == 1) return HB_OK;
+  if (is_ipc(op)) return ipc_allreduce(op, v, st);
   NC_TRY(ncclAllReduce(v, v, 1, ncclFloat64, ncclSum, op->comm->nccl, st));
   return HB_OK;
 }
@@ -518,6 +636,7 @@ int apply_internal(hb_op* op, const double* x, double* y, bool init_y, cudaStrea
   const int last = last_launch(op);
   cudaStream_t cs = op->comm_stream;
   auto nccl = [op](int kind, cudaStream_t c) -> int {
+    if (is_ipc(op)) return ipc_exchange(op, kind, c);
     std::vector<Msg> snd, rcv;
     if (kind == 0) halo_msgs(op, snd, rcv); else assembly_msgs(op, snd, rcv);
     return nccl_exchange(op, snd, rcv, c);
@@ -550,6 +669,17 @@ extern "C" int hb_comm_create(int P, int rank, const uint8_t id[128], hb_comm** 
   std::memcpy(&u, id, 128);
   ncclResult_t r = ncclCommInitRank(&c->nccl, P, u, rank);
   if (r != ncclSuccess) { set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); delete c; return HB_ERR_NCCL; }
+  *out = c;
+  return HB_OK;
+}
+
+extern "C" int hb_comm_create_ipc(int P, int rank, hb_comm** out) {
+  if (!out || P < 1 || P > 32 || rank < 0 || rank >= P) { set_error("hb_comm_create_ipc: bad argument (1 <= P <= 32)"); return HB_ERR_ARG; }
+  *out = nullptr;
+  if (P > 1) HB_TRY(load_memops());
+  auto* c = new (std::nothrow) hb_comm();
+  if (!c) { set_error("hb_comm_create_ipc: out of memory"); return HB_ERR_OOM; }
+  c->P = P; c->rank = rank; c->kind = 1;
   *out = c;
   return HB_OK;
 }
@@ -686,6 +816,11 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     int lo, hi;
     CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU_TRY(cudaStreamCreateWithPriority(&op->comm_stream, cudaStreamNonBlocking, hi));
+    if (comm->kind == 1) {  // IPC mailbox (zeroed before it is exported) and pointer tables
+      HB_TRY(op->mbox.alloc(mbox_bytes(m->P)));
+      CU_TRY(cudaMemsetAsync(op->mbox.p, 0, mbox_bytes(m->P), st));
+      HB_TRY(op->ipc_tab.alloc((size_t)2 * m->P * sizeof(void*)));
+    }
   }
   CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
   CU_TRY(cudaStreamCreateWithFlags(&op->cap_stream2, cudaStreamNonBlocking));
@@ -715,6 +850,110 @@ static int check_multi(hb_op* op, const char* fn) {
     set_error(std::string(fn) + ": P>1 op without a communicator (use a loopback group)");
     return HB_ERR_STATE;
   }
+  if (op->sz.P > 1 && is_ipc(op) && !op->ipc_ready) {
+    set_error(std::string(fn) + ": IPC op not connected (call hb_op_ipc_connect on every rank)");
+    return HB_ERR_STATE;
+  }
+  return HB_OK;
+}
+
+// --- IPC bootstrap: export record = header + per-neighbour arrays padded to P entries
+namespace {
+struct IpcHeader {
+  uint32_t magic, P, rank, nn;
+  uint32_t has_xh, has_recv, pad[2];
+  cudaIpcMemHandle_t mbox, xh, recv;
+};
+constexpr uint32_t kIpcMagic = 0x48424950u;  // "HBIP"
+size_t ipc_blob_bytes(int P) { return sizeof(IpcHeader) + (size_t)P * (4 + 4 * 8); }
+}  // namespace
+
+extern "C" int hb_op_ipc_blob_size(const hb_op* op, int64_t* bytes) {
+  if (!op || !bytes) { set_error("hb_op_ipc_blob_size: null pointer"); return HB_ERR_ARG; }
+  if (!is_ipc(op) || op->sz.P < 2) { set_error("hb_op_ipc_blob_size: op is not on a P>1 IPC communicator"); return HB_ERR_STATE; }
+  *bytes = (int64_t)ipc_blob_bytes(op->sz.P);
+  return HB_OK;
+}
+
+extern "C" int hb_op_ipc_export(const hb_op* op, uint8_t* blob) {
+  if (!op || !blob) { set_error("hb_op_ipc_export: null pointer"); return HB_ERR_ARG; }
+  if (!is_ipc(op) || op->sz.P < 2) { set_error("hb_op_ipc_export: op is not on a P>1 IPC communicator"); return HB_ERR_STATE; }
+  const int P = op->sz.P;
+  std::memset(blob, 0, ipc_blob_bytes(P));
+  IpcHeader h{};
+  h.magic = kIpcMagic; h.P = (uint32_t)P; h.rank = (uint32_t)op->sz.rank; h.nn = (uint32_t)op->nbr.size();
+  CU_TRY(cudaIpcGetMemHandle(&h.mbox, op->mbox.p));
+  h.has_xh = op->xh.p != nullptr;
+  h.has_recv = op->recv_buf.p != nullptr;
+  if (h.has_xh) CU_TRY(cudaIpcGetMemHandle(&h.xh, op->xh.p));
+  if (h.has_recv) CU_TRY(cudaIpcGetMemHandle(&h.recv, op->recv_buf.p));
+  std::memcpy(blob, &h, sizeof(h));
+  int32_t* nb = reinterpret_cast<int32_t*>(blob + sizeof(h));
+  int64_t* arr = reinterpret_cast<int64_t*>(blob + sizeof(h) + (size_t)P * 4);  // scnt, soff, rcnt, roff
+  for (size_t i = 0; i < op->nbr.size(); ++i) {
+    nb[i] = op->nbr[i];
+    arr[0 * P + i] = op->scnt[i]; arr[1 * P + i] = op->soff[i];
+    arr[2 * P + i] = op->rcnt[i]; arr[3 * P + i] = op->roff[i];
+  }
+  return HB_OK;
+}
+
+extern "C" int hb_op_ipc_connect(hb_op* op, const uint8_t* blobs) {
+  if (!op || !blobs) { set_error("hb_op_ipc_connect: null pointer"); return HB_ERR_ARG; }
+  if (!is_ipc(op) || op->sz.P < 2) { set_error("hb_op_ipc_connect: op is not on a P>1 IPC communicator"); return HB_ERR_STATE; }
+  if (op->ipc_ready) { set_error("hb_op_ipc_connect: already connected"); return HB_ERR_STATE; }
+  const int P = op->sz.P, me = op->sz.rank;
+  const size_t B = ipc_blob_bytes(P);
+  op->peers.assign(P, hb_op::IpcPeer{});
+  std::vector<void*> vt(2 * (size_t)P, nullptr);
+  auto open = [op](const cudaIpcMemHandle_t& hd, void** out) -> int {
+    CU_TRY(cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess));
+    op->ipc_opened.push_back(*out);
+    return HB_OK;
+  };
+  for (int q = 0; q < P; ++q) {
+    const uint8_t* b = blobs + (size_t)q * B;
+    IpcHeader h;
+    std::memcpy(&h, b, sizeof(h));
+    if (h.magic != kIpcMagic || (int)h.P != P || (int)h.rank != q) {
+      set_error("hb_op_ipc_connect: record " + std::to_string(q) + " is not rank " + std::to_string(q) + "'s export");
+      return HB_ERR_STATE;
+    }
+    hb_op::IpcPeer& pr = op->peers[q];
+    void* mb = nullptr;
+    if (q == me) mb = op->mbox.p;
+    else HB_TRY(open(h.mbox, &mb));
+    pr.flags = static_cast<uint32_t*>(mb);
+    pr.vals = reinterpret_cast<double*>(static_cast<char*>(mb) + mbox_vals_off(P));
+    vt[q] = pr.vals;
+    vt[P + q] = pr.flags + F_AR * P;
+    if (q == me) continue;
+    auto it = std::find(op->nbr.begin(), op->nbr.end(), q);
+    if (it == op->nbr.end()) continue;
+    const size_t i = (size_t)(it - op->nbr.begin());
+    const int32_t* nb = reinterpret_cast<const int32_t*>(b + sizeof(h));
+    const int64_t* arr = reinterpret_cast<const int64_t*>(b + sizeof(h) + (size_t)P * 4);
+    int64_t j = -1;
+    for (uint32_t t = 0; t < h.nn && t < (uint32_t)P; ++t) if (nb[t] == me) j = t;
+    if (j < 0 || arr[2 * P + j] != op->scnt[i] || arr[0 * P + j] != op->rcnt[i]) {
+      set_error("hb_op_ipc_connect: exchange plans of ranks " + std::to_string(me) + " and " + std::to_string(q) + " disagree");
+      return HB_ERR_STATE;
+    }
+    if (op->scnt[i]) {  // this rank writes into q's xh
+      void* p = nullptr;
+      HB_TRY(open(h.xh, &p));
+      pr.xh = static_cast<double*>(p);
+      pr.xh_off = arr[3 * P + j];
+    }
+    if (op->rcnt[i]) {  // this rank writes into q's recv
+      void* p = nullptr;
+      HB_TRY(open(h.recv, &p));
+      pr.recv = static_cast<double*>(p);
+      pr.recv_off = arr[1 * P + j];
+    }
+  }
+  CU_TRY(cudaMemcpy(op->ipc_tab.p, vt.data(), vt.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  op->ipc_ready = true;
   return HB_OK;
 }
 
@@ -823,7 +1062,7 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   op->launches++;
   CU_TRY(cudaEventRecord(op->ev_red, st));
   CU_TRY(cudaStreamWaitEvent(op->comm_stream, op->ev_red, 0));
-  NC_TRY(ncclAllReduce(&s->rr_new, &s->rr_new, 1, ncclFloat64, ncclSum, op->comm->nccl, op->comm_stream));
+  HB_TRY(allreduce_sum(op, &s->rr_new, op->comm_stream));
   CU_TRY(cudaEventRecord(op->ev_red_done, op->comm_stream));
   hbk::cg_update_x<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), n, s);
   op->launches++;
@@ -888,6 +1127,12 @@ int finish_result(hb_op* op, int32_t iters, double* rr_hist_host, hb_cg_result* 
 int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_host, hb_cg_result* res,
              cudaStream_t st) {
   HB_TRY(ensure_hist(op, K));
+  if (is_ipc(op)) {  // stream-ordered loop: the transport's flags carry per-call sequence numbers
+    if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }
+    HB_TRY(cg_init(op, b, x, st));
+    for (int32_t j = 0; j < K; ++j) HB_TRY(cg_iteration(op, x, st));
+    return finish_result(op, K, rr_hist_host, res, st);
+  }
   hb_op::GraphKey key{K, b, x, op->profiling, st};
   auto it = op->graphs.find(key);
   if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }  // a profiling graph records into events 0..n-1

@@ -566,4 +566,24 @@ unpack_add_kernel(double* __restrict__ y, const int32_t* __restrict__ loc, const
     atomicAdd(y + loc[t], buf[t]);
 }
 
+// IPC allreduce (op.cu ipc_allreduce): lane q stores this rank's value into rank q's mailbox
+// slot vals[q][slot*P + me] (peer memory), then -- after a system-scope fence -- raises this
+// rank's flag in rank q's mailbox to seq.  vals_tab / flag_tab: per-rank base pointers
+// (peer-mapped, own entry local); P <= 32.
+__global__ void ipc_push_kernel(const double* __restrict__ v, double* const* __restrict__ vals_tab,
+                                uint32_t* const* __restrict__ flag_tab, int P, int me, int slot, uint32_t seq) {
+  const int q = threadIdx.x;
+  if (q >= P) return;
+  vals_tab[q][slot * P + me] = *v;
+  __threadfence_system();
+  if (q != me) *(volatile uint32_t*)(flag_tab[q] + me) = seq;
+}
+
+// sum of the P slot values in rank order (identical on every rank: deterministic allreduce)
+__global__ void ipc_sum_kernel(const double* vals, int P, double* out) {
+  double s = 0.0;
+  for (int q = 0; q < P; ++q) s += ((const volatile double*)vals)[q];
+  *out = s;
+}
+
 }  // namespace hbk

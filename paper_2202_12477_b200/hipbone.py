@@ -77,6 +77,10 @@ _SIGS = {
     "hb_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "hb_comm_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(_p)]),
     "hb_comm_destroy": (C.c_int, [_p]),
+    "hb_comm_create_ipc": (C.c_int, [C.c_int, C.c_int, C.POINTER(_p)]),
+    "hb_op_ipc_blob_size": (C.c_int, [_p, _i64p]),
+    "hb_op_ipc_export": (C.c_int, [_p, C.POINTER(C.c_uint8)]),
+    "hb_op_ipc_connect": (C.c_int, [_p, C.POINTER(C.c_uint8)]),
     "hb_op_create": (C.c_int, [_p, _p, C.c_double, _p, C.POINTER(_p)]),
     "hb_op_apply": (C.c_int, [_p, _p, _p, _p]),
     "hb_forcing": (C.c_int, [_p, C.c_uint64, _p, _p]),
@@ -241,13 +245,22 @@ def comm_unique_id() -> bytes:
 
 
 class Comm:
-    """NCCL communicator (one GPU per rank)."""
+    """Communicator of one rank: NCCL (`Comm(P, rank, uid)`, one GPU per rank) or the IPC
+    peer-memory transport (`Comm.ipc(P, rank)`; ops on it need `Operator.ipc_connect`)."""
 
-    def __init__(self, P: int, rank: int, uid: bytes):
-        a = (C.c_uint8 * 128).from_buffer_copy(uid)
+    def __init__(self, P: int, rank: int, uid: bytes | None = None, *, ipc: bool = False):
         h = _p()
-        _check(_lib.hb_comm_create(P, rank, a, C.byref(h)))
+        if ipc:
+            _check(_lib.hb_comm_create_ipc(P, rank, C.byref(h)))
+        else:
+            a = (C.c_uint8 * 128).from_buffer_copy(uid)
+            _check(_lib.hb_comm_create(P, rank, a, C.byref(h)))
         self._h = h
+        self.ipc = ipc
+
+    @classmethod
+    def create_ipc(cls, P: int, rank: int) -> "Comm":
+        return cls(P, rank, ipc=True)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -273,6 +286,20 @@ class Operator:
         if getattr(self, "_h", None):
             _lib.hb_op_destroy(self._h)
             self._h = None
+
+    def ipc_export(self) -> bytes:
+        """This rank's IPC export record (hb_op_ipc_export)."""
+        n = C.c_int64()
+        _check(_lib.hb_op_ipc_blob_size(self._h, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        _check(_lib.hb_op_ipc_export(self._h, buf))
+        return bytes(buf)
+
+    def ipc_connect(self, records) -> None:
+        """Map the peers' buffers from the all-gathered records (rank order; hb_op_ipc_connect)."""
+        blob = b"".join(records)
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(_lib.hb_op_ipc_connect(self._h, buf))
 
     def apply(self, x, y, stream=None):
         _check(_lib.hb_op_apply(self._h, _dev(x), _dev(y), _stream(stream)))

@@ -1,0 +1,33 @@
+"""Multi-process parity of the IPC peer-memory transport (hb_comm_create_ipc, SURVEY §8(f)
+NEXT #2): P torchrun processes share the one GPU of the test box (NCCL refuses that; the IPC
+transport's exchanges and allreduces do not care), each runs its partition's split operator,
+a dot, fixed- and tolerance-mode CG; rank 0 checks the assembled results against the oracle
+(c17 apply tolerance, c18 CG history / iteration count).  scripts/multirank_selftest.py."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(P, box, N, port):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, "scripts", "multirank_selftest.py"), "--transport", "ipc",
+           "--box", ",".join(map(str, box)), "--N", str(N)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and lines, f"rc={r.returncode}\n{r.stdout[-3000:]}\n{r.stderr[-3000:]}"
+    return json.loads(lines[-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,box,N,port", [(2, (4, 3, 4), 3, 29611), (4, (5, 4, 3), 2, 29612),
+                                           (3, (6, 2, 2), 5, 29613)])
+def test_ipc_transport_parity(P, box, N, port):
+    out = _run(P, box, N, port)
+    assert "error" not in out, out
+    assert out["ok"], out
