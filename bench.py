@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--jacobi", action="store_true", help="Jacobi-preconditioned CG (P=1; not the NekBone FOM)")
     ap.add_argument("--storage", default="assembled", choices=["assembled", "scattered"],
                     help="scattered = NekBone's x_L storage with weighted dots (P=1 experiment, P:112-121)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="P>1 exchanges/allreduces: NCCL, or the IPC peer-memory transport (several ranks may share a GPU)")
     return ap.parse_args()
 
 
@@ -187,9 +189,13 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local_rank)
+    ipc = args.transport == "ipc"
+    torch.cuda.set_device(local_rank % torch.cuda.device_count() if ipc else local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if ipc:  # bootstrap only (records, barriers, the max over ranks); the data path is the library's
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     import __graft_entry__
     if rank == 0:
@@ -205,14 +211,21 @@ def main():
     if world > 1:
         grid = hb.rank_grid(world, 64, 64, 64)  # rank grid shape only (px >= py >= pz)
         box = (blk[0] * grid[0], blk[1] * grid[1], blk[2] * grid[2])
-        uid = [hb.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = hb.Comm(world, rank, uid[0])
+        if ipc:
+            comm = hb.Comm.create_ipc(world, rank)
+        else:
+            uid = [hb.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = hb.Comm(world, rank, uid[0])
         mesh = hb.Mesh(*box, N, P=world, rank=rank, grid=grid)
     else:
         box = blk
         mesh = hb.Mesh(*box, N)
     op = hb.Operator(mesh, lam=1.0, comm=comm)
+    if world > 1 and ipc:
+        recs = [None] * world
+        dist.all_gather_object(recs, op.ipc_export())
+        op.ipc_connect(recs)
     if args.variant:
         op.set_variant(args.variant)
     if args.jacobi:
@@ -267,7 +280,8 @@ def main():
     launches = op.launch_count() - l0
     step_ms = [a.elapsed_time(bv) for a, bv in ev]
     my_ms = sum(step_ms) / len(step_ms)
-    tmax = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
+    rdev = "cpu" if ipc else "cuda"
+    tmax = torch.tensor([my_ms], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = tmax.item()
@@ -292,7 +306,7 @@ def main():
         t0 = time.perf_counter()
         op.cg_host(bnp, xnp, K, hist=False)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_t = torch.tensor([sum(e2e_ms) / max(len(e2e_ms), 1)], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([sum(e2e_ms) / max(len(e2e_ms), 1)], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (e2e_t.item() * 1e-3) / 1e9 if e2e_ms else None
@@ -335,6 +349,7 @@ def main():
                           "iterations": K, "lambda": 1.0, "mass_mode": 0, "forcing_seed": 1,
                           "l2": "flushed between steps (256 MiB write); working set > L2",
                           "parallelism": f"element partition p{world}",
+                          "transport": (args.transport if world > 1 else None),
                           "assembly_variant": args.variant, "preconditioner": "jacobi" if args.jacobi else "none",
                           "storage": args.storage},
                "gdofs_per_s": round(gdofs, 4),
