@@ -161,6 +161,14 @@ int hb_op_apply(hb_op* op, const double* x_dev, double* y_dev, void* stream);
 int hb_op_ipc_blob_size(const hb_op* op, int64_t* bytes);
 int hb_op_ipc_export(const hb_op* op, uint8_t* blob);
 int hb_op_ipc_connect(hb_op* op, const uint8_t* blobs);
+/* IPC direct mode for CG (default on): the halo-element kernel reads the owners' p and
+ * scatter-adds (fp64 RED) into the owners' Ap through per-halo-node peer pointers, so the
+ * operator of a CG iteration needs no exchange, pack or unpack -- the collective is fused into
+ * the compute kernel.  Ordering: per iteration each owner raises RDY after writing p and
+ * Ap = lambda p; each sharer waits RDY before its halo elements and raises DONE after them;
+ * the owner waits DONE before reading Ap.  enable = 0 selects the exchange path (as
+ * hb_op_apply always uses).  Collective: all ranks must use the same setting. */
+int hb_op_set_ipc_direct(hb_op* op, int enable);
 /* b_dev[l] = forcing(owned_gid[l], seed) (c12), [n_owned].  Asynchronous. */
 int hb_forcing(hb_op* op, uint64_t seed, double* b_dev, void* stream);
 /* global a.b over owned DOFs (allreduced for P>1); synchronises the stream. */

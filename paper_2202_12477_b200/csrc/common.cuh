@@ -38,6 +38,8 @@ struct AxArgs {
   //  operator's code generation -- 10% slower at N = 7)
   int64_t e_begin, e_end;           // element range of this launch
   int32_t n_owned;
+  int32_t halo_mode;                // HALO kernels: 0 xh / yh arrays; 1 xh / yh hold per-halo-node
+                                    // pointers into the owners' p / Ap (IPC direct mode, peer memory)
   double lam;
   // fused p.Ap (CG only; cg == nullptr otherwise): p.Ap = sum_e u_e^T S_e u_e + lambda p.p
   CgScalars* cg;
@@ -49,16 +51,27 @@ struct AxArgs {
                     // the x/r update kernel reduces them (no fence/atomic in the operator)
 };
 
+static_assert(sizeof(AxArgs) == 128, "AxArgs must stay at 128 bytes (see the comment in the struct)");
+
 template <bool HALO>
 __device__ __forceinline__ double load_x(const AxArgs& a, int32_t g) {
-  if (HALO && g >= a.n_owned) return a.xh[g - a.n_owned];
+  if (HALO && g >= a.n_owned) {
+    const int32_t h = g - a.n_owned;
+    if (a.halo_mode) return *reinterpret_cast<const double* const*>(a.xh)[h];  // owner's p (peer memory)
+    return a.xh[h];
+  }
   return __ldg(a.x + g);
 }
 
 template <bool HALO>
 __device__ __forceinline__ void red_y(const AxArgs& a, int32_t g, double v) {
-  if (HALO && g >= a.n_owned) atomicAdd(a.yh + (g - a.n_owned), v);
-  else atomicAdd(a.y + g, v);
+  if (HALO && g >= a.n_owned) {
+    const int32_t h = g - a.n_owned;
+    if (a.halo_mode) atomicAdd(reinterpret_cast<double* const*>(a.yh)[h], v);  // owner's Ap (peer memory)
+    else atomicAdd(a.yh + h, v);
+  } else {
+    atomicAdd(a.y + g, v);
+  }
 }
 
 // L2 prefetch of a contiguous byte range by the bulk-copy engine (sm_90+): no registers,

@@ -315,6 +315,12 @@ struct hb_op {
   std::vector<IpcPeer> peers;
   std::vector<void*> ipc_opened;
   uint32_t apply_seq = 0, ar_seq = 0;
+  // IPC direct mode (CG): the halo-element kernel reads the owners' p and scatter-adds into
+  // the owners' Ap through per-halo-node peer pointers -- no exchange, no pack / unpack
+  bool ipc_direct = true;
+  DevBuf hx_tab, hy_tab;   // [n_halo] pointers into the owners' p / Ap
+  uint32_t iter_seq = 0;   // direct-mode CG iterations so far (RDY / DONE flag values)
+  int halo_mode_now = 0;   // launch_ax: pass the pointer tables to the HALO kernel
   ~hb_op() {
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -367,6 +373,12 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   if (op->scat_mode) a.xh = op->sL_p.as<double>();                     // ASM == 2 reads x_L there
   a.e_begin = e0; a.e_end = e1;
   a.n_owned = (int32_t)op->sz.n_owned;
+  a.halo_mode = 0;
+  if (op->halo_mode_now) {
+    a.halo_mode = 1;
+    a.xh = op->hx_tab.as<double>();
+    a.yh = op->hy_tab.as<double>();
+  }
   a.lam = op->lam;
   a.cg = energy ? op->scal.as<hbk::CgScalars>() : nullptr;
   a.e_part = op->e_part.as<double>();
@@ -426,8 +438,11 @@ int phase_event(hb_op* op, hb_op::Timer& tm, bool start, cudaStream_t st) {
 // of the next apply).  Allreduce: every rank stores its value into slot [s & 1][me] of every
 // mailbox and raises AR = s; two slots suffice because no rank can start allreduce s + 2
 // before every rank has finished s (it needs their s + 1 values, pushed after their sum of s).
-// Mailbox layout: uint32 flags[5][P] (indexed by source rank), then double vals[2][P].
-enum { F_HD = 0, F_HF = 1, F_AD = 2, F_AF = 3, F_AR = 4, F_KINDS = 5 };
+// Direct mode (CG, hb_op_set_ipc_direct): RDY (owner's p and Ap = lambda p of iteration it are
+// written, = it) and DONE (sharer's halo elements of iteration it have read p and added into
+// Ap, = it) replace both exchanges.
+// Mailbox layout: uint32 flags[7][P] (indexed by source rank), then double vals[2][P].
+enum { F_HD = 0, F_HF = 1, F_AD = 2, F_AF = 3, F_AR = 4, F_RDY = 5, F_DONE = 6, F_KINDS = 7 };
 size_t mbox_vals_off(int P) { return ((size_t)F_KINDS * P * 4 + 255) & ~size_t(255); }
 size_t mbox_bytes(int P) { return mbox_vals_off(P) + (size_t)2 * P * 8; }
 
@@ -514,6 +529,16 @@ int ipc_allreduce(hb_op* op, double* v, cudaStream_t st) {
   hbk::ipc_sum_kernel<<<1, 1, 0, st>>>(vals + slot * P, P, v);
   op->launches++;
   CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+bool direct_mode(const hb_op* op) { return is_ipc(op) && op->comm->P > 1 && op->ipc_direct; }
+
+// owners of this rank's halo nodes (rcnt > 0) / sharers of its owned nodes (scnt > 0)
+int ipc_signal_ready(hb_op* op, cudaStream_t st) {  // p and Ap init of the next iteration written
+  const int P = op->comm->P, me = op->comm->rank;
+  for (size_t i = 0; i < op->nbr.size(); ++i)
+    if (op->scnt[i]) HB_TRY(mem_signal(st, op->peers[op->nbr[i]].flags + F_RDY * P + me, op->iter_seq + 1));
   return HB_OK;
 }
 
@@ -611,6 +636,34 @@ int rank_phase_assembly(hb_op* op, const double* x, double* y, cudaStream_t st, 
 int last_launch(const hb_op* op) {  // the last non-empty launch publishes p.Ap
   const int64_t nB = op->sz.E_local - op->nA - op->nH;
   return nB > 0 ? 2 : (op->nH > 0 ? 1 : 0);
+}
+
+// Direct-mode operator of a CG iteration (IPC, P > 1): Ap += A p with Ap = lambda p already
+// written by the p update.  Interior elements first (they overlap the neighbours' progress),
+// then -- once every owner of a halo node has published p (RDY) -- the halo elements, which
+// read the owners' p and RED into the owners' Ap over peer memory; finally wait until every
+// sharer of an owned node has done the same (DONE) before the vector update reads Ap.
+int direct_apply(hb_op* op, cudaStream_t st) {
+  const int P = op->comm->P, me = op->comm->rank;
+  const uint32_t it = ++op->iter_seq;
+  const int64_t E = op->sz.E_local, a0 = op->nA, h0 = op->nA, h1 = op->nA + op->nH;
+  const int last = op->nH > 0 ? 1 : (E - h1 > 0 ? 2 : 0);
+  const double* p = op->p.as<double>();
+  double* Ap = op->Ap.as<double>();
+  uint32_t* own = op->mbox.as<uint32_t>();
+  HB_TRY(launch_ax(op, op->ax_plain, 0, a0, p, Ap, st, true, last == 0));
+  HB_TRY(launch_ax(op, op->ax_plain, h1, E, p, Ap, st, true, last == 2));
+  for (size_t i = 0; i < op->nbr.size(); ++i)
+    if (op->rcnt[i]) HB_TRY(mem_wait(st, own + F_RDY * P + op->nbr[i], it));
+  op->halo_mode_now = 1;
+  const int hs = launch_ax(op, op->ax_halo, h0, h1, p, Ap, st, true, last == 1);
+  op->halo_mode_now = 0;
+  HB_TRY(hs);
+  for (size_t i = 0; i < op->nbr.size(); ++i)
+    if (op->rcnt[i]) HB_TRY(mem_signal(st, op->peers[op->nbr[i]].flags + F_DONE * P + me, it));
+  for (size_t i = 0; i < op->nbr.size(); ++i)
+    if (op->scnt[i]) HB_TRY(mem_wait(st, own + F_DONE * P + op->nbr[i], it));
+  return HB_OK;
 }
 
 // y = A x for one op (P = 1, or P > 1 with NCCL).  init_y=false: y already holds the
@@ -861,8 +914,9 @@ static int check_multi(hb_op* op, const char* fn) {
 namespace {
 struct IpcHeader {
   uint32_t magic, P, rank, nn;
-  uint32_t has_xh, has_recv, pad[2];
-  cudaIpcMemHandle_t mbox, xh, recv;
+  uint32_t has_xh, has_recv, has_send_loc, pad;
+  int64_t off_p, off_Ap;  // byte offsets of p and Ap in the arena allocation (direct mode)
+  cudaIpcMemHandle_t mbox, xh, recv, arena, send_loc;
 };
 constexpr uint32_t kIpcMagic = 0x48424950u;  // "HBIP"
 size_t ipc_blob_bytes(int P) { return sizeof(IpcHeader) + (size_t)P * (4 + 4 * 8); }
@@ -887,6 +941,11 @@ extern "C" int hb_op_ipc_export(const hb_op* op, uint8_t* blob) {
   h.has_recv = op->recv_buf.p != nullptr;
   if (h.has_xh) CU_TRY(cudaIpcGetMemHandle(&h.xh, op->xh.p));
   if (h.has_recv) CU_TRY(cudaIpcGetMemHandle(&h.recv, op->recv_buf.p));
+  h.has_send_loc = op->send_loc.p != nullptr;
+  if (h.has_send_loc) CU_TRY(cudaIpcGetMemHandle(&h.send_loc, op->send_loc.p));
+  CU_TRY(cudaIpcGetMemHandle(&h.arena, op->arena.p));
+  h.off_p = op->p.as<char>() - op->arena.as<char>();
+  h.off_Ap = op->Ap.as<char>() - op->arena.as<char>();
   std::memcpy(blob, &h, sizeof(h));
   int32_t* nb = reinterpret_cast<int32_t*>(blob + sizeof(h));
   int64_t* arr = reinterpret_cast<int64_t*>(blob + sizeof(h) + (size_t)P * 4);  // scnt, soff, rcnt, roff
@@ -898,6 +957,13 @@ extern "C" int hb_op_ipc_export(const hb_op* op, uint8_t* blob) {
   return HB_OK;
 }
 
+extern "C" int hb_op_set_ipc_direct(hb_op* op, int enable) {
+  if (!op) { set_error("hb_op_set_ipc_direct: null pointer"); return HB_ERR_ARG; }
+  if (!is_ipc(op)) { set_error("hb_op_set_ipc_direct: op is not on an IPC communicator"); return HB_ERR_STATE; }
+  op->ipc_direct = enable != 0;
+  return HB_OK;
+}
+
 extern "C" int hb_op_ipc_connect(hb_op* op, const uint8_t* blobs) {
   if (!op || !blobs) { set_error("hb_op_ipc_connect: null pointer"); return HB_ERR_ARG; }
   if (!is_ipc(op) || op->sz.P < 2) { set_error("hb_op_ipc_connect: op is not on a P>1 IPC communicator"); return HB_ERR_STATE; }
@@ -906,6 +972,7 @@ extern "C" int hb_op_ipc_connect(hb_op* op, const uint8_t* blobs) {
   const size_t B = ipc_blob_bytes(P);
   op->peers.assign(P, hb_op::IpcPeer{});
   std::vector<void*> vt(2 * (size_t)P, nullptr);
+  std::vector<double*> hx((size_t)op->sz.n_halo, nullptr), hy((size_t)op->sz.n_halo, nullptr);
   auto open = [op](const cudaIpcMemHandle_t& hd, void** out) -> int {
     CU_TRY(cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess));
     op->ipc_opened.push_back(*out);
@@ -945,12 +1012,32 @@ extern "C" int hb_op_ipc_connect(hb_op* op, const uint8_t* blobs) {
       pr.xh = static_cast<double*>(p);
       pr.xh_off = arr[3 * P + j];
     }
-    if (op->rcnt[i]) {  // this rank writes into q's recv
+    if (op->rcnt[i]) {  // this rank writes into q's recv; direct mode reads q's p, adds into q's Ap
       void* p = nullptr;
       HB_TRY(open(h.recv, &p));
       pr.recv = static_cast<double*>(p);
       pr.recv_off = arr[1 * P + j];
+      void* ar = nullptr;
+      void* sl = nullptr;
+      HB_TRY(open(h.arena, &ar));
+      if (!h.has_send_loc) { set_error("hb_op_ipc_connect: owner without a send list"); return HB_ERR_STATE; }
+      HB_TRY(open(h.send_loc, &sl));
+      // q's send list for this rank is in the order of this rank's xh segment from q (gid order)
+      std::vector<int32_t> loc((size_t)op->rcnt[i]);
+      CU_TRY(cudaMemcpy(loc.data(), static_cast<int32_t*>(sl) + arr[1 * P + j], loc.size() * 4, cudaMemcpyDeviceToHost));
+      for (size_t t = 0; t < loc.size(); ++t) {
+        hx[(size_t)op->roff[i] + t] = reinterpret_cast<double*>(static_cast<char*>(ar) + h.off_p) + loc[t];
+        hy[(size_t)op->roff[i] + t] = reinterpret_cast<double*>(static_cast<char*>(ar) + h.off_Ap) + loc[t];
+      }
     }
+  }
+  for (size_t t = 0; t < hx.size(); ++t)
+    if (!hx[t]) { set_error("hb_op_ipc_connect: halo node without an owner mapping"); return HB_ERR_STATE; }
+  if (!hx.empty()) {
+    HB_TRY(op->hx_tab.alloc(hx.size() * sizeof(double*)));
+    HB_TRY(op->hy_tab.alloc(hy.size() * sizeof(double*)));
+    CU_TRY(cudaMemcpy(op->hx_tab.p, hx.data(), hx.size() * sizeof(double*), cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemcpy(op->hy_tab.p, hy.data(), hy.size() * sizeof(double*), cudaMemcpyHostToDevice));
   }
   CU_TRY(cudaMemcpy(op->ipc_tab.p, vt.data(), vt.size() * sizeof(void*), cudaMemcpyHostToDevice));
   op->ipc_ready = true;
@@ -1009,7 +1096,9 @@ int cg_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
   op->launches++;
   CU_TRY(cudaGetLastError());
   hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
-  return allreduce_sum(op, &s->rr_new, st);
+  HB_TRY(allreduce_sum(op, &s->rr_new, st));
+  if (direct_mode(op)) HB_TRY(ipc_signal_ready(op, st));  // p = b and Ap = lambda p are written
+  return HB_OK;
 }
 
 // One CG iteration after the operator (which published p.Ap): x/r update + r.r, then p update.
@@ -1089,6 +1178,12 @@ int cg_vec_part2(hb_op* op, cudaStream_t st) {
 }
 
 int cg_iteration(hb_op* op, double* x, cudaStream_t st) {
+  if (direct_mode(op)) {
+    HB_TRY(direct_apply(op, st));
+    HB_TRY(cg_vec_part1(op, x, st));
+    HB_TRY(cg_vec_part2(op, st));
+    return ipc_signal_ready(op, st);
+  }
   HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
   HB_TRY(cg_vec_part1(op, x, st));
   return cg_vec_part2(op, st);
@@ -1259,7 +1354,8 @@ int cg_tol(hb_op* op, const double* b, double* x, int32_t max_iters, double eps,
   int32_t j = 0;
   double rr = hs->rr_new;
   while (j < max_iters && rr > eps) {
-    HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
+    if (direct_mode(op)) HB_TRY(direct_apply(op, st));
+    else HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
     HB_TRY(cg_vec_part1(op, x, st));
     CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaStreamSynchronize(st));
@@ -1268,6 +1364,7 @@ int cg_tol(hb_op* op, const double* b, double* x, int32_t max_iters, double eps,
       return HB_ERR_BREAKDOWN;
     }
     HB_TRY(cg_vec_part2(op, st));
+    if (direct_mode(op)) HB_TRY(ipc_signal_ready(op, st));
     ++j;
     rr = hs->rr_new;
   }

@@ -81,6 +81,7 @@ _SIGS = {
     "hb_op_ipc_blob_size": (C.c_int, [_p, _i64p]),
     "hb_op_ipc_export": (C.c_int, [_p, C.POINTER(C.c_uint8)]),
     "hb_op_ipc_connect": (C.c_int, [_p, C.POINTER(C.c_uint8)]),
+    "hb_op_set_ipc_direct": (C.c_int, [_p, C.c_int]),
     "hb_op_create": (C.c_int, [_p, _p, C.c_double, _p, C.POINTER(_p)]),
     "hb_op_apply": (C.c_int, [_p, _p, _p, _p]),
     "hb_forcing": (C.c_int, [_p, C.c_uint64, _p, _p]),
@@ -300,6 +301,10 @@ class Operator:
         blob = b"".join(records)
         buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
         _check(_lib.hb_op_ipc_connect(self._h, buf))
+
+    def set_ipc_direct(self, enable: bool) -> None:
+        """IPC transport, CG: halo elements read / add into the owners' vectors directly (default)."""
+        _check(_lib.hb_op_set_ipc_direct(self._h, int(bool(enable))))
 
     def apply(self, x, y, stream=None):
         _check(_lib.hb_op_apply(self._h, _dev(x), _dev(y), _stream(stream)))

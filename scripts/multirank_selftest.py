@@ -60,13 +60,20 @@ def main():
         x = torch.zeros_like(b)
         op.forcing(1, b)
         K = 20
-        j, hist = op.cg(b, x, K)
-        x2 = torch.zeros_like(b)
-        j2, hist2 = op.cg(b, x2, 400, eps=1e-12)  # tolerance mode (host-driven loop for P > 1)
+        modes = [True, False] if a.transport == "ipc" else [None]
+        runs = []
+        for direct in modes:  # IPC: direct (peer-memory halo elements) and exchange CG
+            if direct is not None:
+                op.set_ipc_direct(direct)
+            x = torch.zeros_like(b)
+            j, hist = op.cg(b, x, K)
+            x2 = torch.zeros_like(b)
+            j2, hist2 = op.cg(b, x2, 400, eps=1e-12)  # tolerance mode (host-driven loop for P > 1)
+            runs.append((j, hist, x.cpu().numpy(), j2, hist2))
         op.apply(b, y)                               # re-apply after the solves: sequence numbers advance
         torch.cuda.synchronize()
         gathered = [None] * P
-        dist.all_gather_object(gathered, (m.owned(), y.cpu().numpy(), x.cpu().numpy()))
+        dist.all_gather_object(gathered, (m.owned(), y.cpu().numpy(), [r[2] for r in runs]))
         if rank == 0:
             from oracle import basis, cg as ocg, forcing as of, mesh as om, operator as oo
             xg, w, D = basis.basis(N)
@@ -80,20 +87,25 @@ def main():
             yo = A(b1)
             s = oo.apply_abs(b1, gid, D, G, 1.0, W)
             yg = np.zeros(NG)
-            xgv = np.zeros(NG)
-            for own, yy, xx in gathered:
+            for own, yy, _ in gathered:
                 yg[own] = yy
-                xgv[own] = xx
             xo, _, ho = ocg.cg(A, b1, max_iters=K)
             _, jo2, ho2 = ocg.cg(A, b1, max_iters=400, eps=1e-12)
             out.update(apply_err=float(np.max(np.abs(yg - yo) / s)),
-                       dot_rel=abs(bb - ocg.dot(b2, b2)) / ocg.dot(b2, b2),
-                       cg_hist_rel=float(np.max(np.abs(hist - np.array(ho)) / np.array(ho))),
-                       x_rel=float(np.max(np.abs(xgv - xo)) / np.max(np.abs(xo))), iterations=j,
-                       tol_iterations=j2, tol_iterations_oracle=jo2,
-                       tol_hist_rel=float(np.max(np.abs(np.array(hist2[:j2]) - np.array(ho2[:j2])) / np.array(ho2[:j2]))))
-            out["ok"] = (out["apply_err"] <= 1e-12 and out["cg_hist_rel"] <= 1e-8 and out["x_rel"] <= 1e-10
-                         and j2 == jo2 and out["tol_hist_rel"] <= 1e-8)
+                       dot_rel=abs(bb - ocg.dot(b2, b2)) / ocg.dot(b2, b2), modes=[])
+            ok = out["apply_err"] <= 1e-12
+            for mi, (direct, (j, hist, _, j2, hist2)) in enumerate(zip(modes, runs)):
+                xgv = np.zeros(NG)
+                for own, _, xs in gathered:
+                    xgv[own] = xs[mi]
+                r = dict(direct=direct, cg_hist_rel=float(np.max(np.abs(hist - np.array(ho)) / np.array(ho))),
+                         x_rel=float(np.max(np.abs(xgv - xo)) / np.max(np.abs(xo))), iterations=j,
+                         tol_iterations=j2, tol_iterations_oracle=jo2,
+                         tol_hist_rel=float(np.max(np.abs(np.array(hist2[:j2]) - np.array(ho2[:j2]))
+                                                   / np.array(ho2[:j2]))))
+                out["modes"].append(r)
+                ok = ok and r["cg_hist_rel"] <= 1e-8 and r["x_rel"] <= 1e-10 and j2 == jo2 and r["tol_hist_rel"] <= 1e-8
+            out["ok"] = bool(ok)
     except Exception as ex:
         out["error"] = repr(ex)
     if rank == 0:
