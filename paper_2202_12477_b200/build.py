@@ -35,6 +35,7 @@ def _compile(src: str, nccl: str, extra: list[str]) -> str:
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
            "-Xptxas", "-v" if os.environ.get("HB_PTXAS_V") else "-O3",
            *(["-DHB_TUNE"] if os.environ.get("HB_TUNE") else []),
+           *([f"-DHB_TUNE_N={int(os.environ['HB_TUNE_N'])}"] if os.environ.get("HB_TUNE") and os.environ.get("HB_TUNE_N") else []),
            *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -148,6 +148,10 @@ AxKernel tune_variant(int v) {
 }
 
 AxKernel pick_ax_variant(int N, int v) {
+#ifdef HB_TUNE_N  // one degree only (faster tuning builds)
+  if (N == HB_TUNE_N) return tune_variant<HB_TUNE_N>(v);
+  return make_lines<7, false, false, 0>();
+#endif
   switch (N) {
     case 1: return tune_variant<1>(v);
     case 2: return tune_variant<2>(v);

@@ -64,6 +64,7 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", default="", help="variants to try per N, e.g. 0,1,2 (needs an HB_TUNE build)")
     ap.add_argument("--degrees", default="", help="comma list of N for --sweep/--tune (default 1..15)")
+    ap.add_argument("--tune-box", default="", help="box for --tune instead of the C3 box, e.g. 16,16,16")
     a = ap.parse_args()
     import __graft_entry__
     __graft_entry__.build()
@@ -73,11 +74,12 @@ def main():
     if a.tune:
         for N in degrees:
             n = C3[N]
+            tb = tuple(int(v) for v in a.tune_box.split(",")) if a.tune_box else (n, n, n)
             for v in a.tune.split(","):
                 os.environ["HB_AX_VN"] = str(N)
                 os.environ["HB_AX_VARIANT"] = v
                 try:
-                    run(N, (n, n, n), a.reps, peak)
+                    run(N, tb, a.reps, peak)
                 except Exception as ex:  # a variant may not launch (resources): report and go on
                     print(json.dumps({"N": N, "variant": v, "error": repr(ex)}), flush=True)
         return
