@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-profile", action="store_true", help="do not bracket operator launches with events")
-    ap.add_argument("--variant", type=int, default=0, help="assembly: 0 fused scatter-add, 1 y_L + CSR (P=1)")
+    ap.add_argument("--variant", type=int, default=0, help="0 fused scatter-add, 1 y_L + CSR (P=1), 2 fused p update (P=1)")
     ap.add_argument("--jacobi", action="store_true", help="Jacobi-preconditioned CG (P=1; not the NekBone FOM)")
     ap.add_argument("--storage", default="assembled", choices=["assembled", "scattered"],
                     help="scattered = NekBone's x_L storage with weighted dots (P=1 experiment, P:112-121)")

@@ -197,8 +197,14 @@ int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t ma
 /* Assembly variant: 0 (default) = Z^T fused into the operator as fp64 scatter-add (atomic
  * accumulation order, results reproducible to rounding); 1 = the paper's split form (P:154,
  * P:219): the operator writes y_L per slot and a CSR gather kernel sums every DOF's slots in
- * ascending (e, n) order -- bitwise reproducible, +20 N_L bytes per apply.  P = 1 only
- * (HB_ERR_STATE otherwise).  Synchronous (builds the CSR on first use). */
+ * ascending (e, n) order -- bitwise reproducible, +20 N_L bytes per apply; 2 = as 0, and
+ * fixed-mode CG moves Alg. 1's p update into the next operator: its gather forms
+ * p_j = r_j + beta_j p_{j-1} from r and the previous p (two alternating buffers), the first
+ * slot (e, n) of every DOF stores p_j and adds lambda W u once (Z^T lambda W Z = lambda I, c1),
+ * and one barrier-free vector kernel does alpha, x, r, r.r, beta and re-zeroes Ap
+ * (96 N_G + 52 N_L bytes per iteration instead of 104 N_G + 52 N_L; same iterates up to
+ * rounding).  Applies and tolerance mode are unchanged.  Variants 1 and 2: P = 1 only
+ * (HB_ERR_STATE otherwise).  Synchronous (builds the CSR / designated slots on first use). */
 int hb_op_set_variant(hb_op* op, int variant, void* stream);
 /* Jacobi-preconditioned CG (NekBone's diagonal preconditioner, P:140 --
  * hipBone itself uses none).  enable = 1 computes M = diag(A) on the device once

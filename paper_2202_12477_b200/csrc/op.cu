@@ -114,6 +114,9 @@ AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
     return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 1>()
                  : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 1>();
   if (asm_mode == 2) return make_lines<N, false, false, kLinesPF, M, 0, PL, true, 2>();  // mass mode 0 only
+  if (asm_mode == 3)
+    return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 3>()
+                 : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 3>();
   return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
 }
 
@@ -271,7 +274,12 @@ struct hb_op {
   std::vector<int64_t> soff, scnt, roff, rcnt;
   int64_t n_send = 0;
   int last_grid = 0;  // grid of the last operator launch (number of energy partials, P = 1)
-  AxKernel ax_plain, ax_halo, ax_yl, ax_scat;  // ax_yl / ax_scat picked on first use
+  AxKernel ax_plain, ax_halo, ax_yl, ax_scat, ax_fp;  // ax_yl / ax_scat / ax_fp picked on first use
+  // fused-p CG (P = 1 fixed mode): the p update runs inside the next operator (ASM == 3)
+  bool fusedp = false;
+  DevBuf idx_des, p_alt;   // idx with the designated-slot sign bit; the second p buffer
+  const double* fp_pold = nullptr;
+  double* fp_pnew = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture (the legacy stream cannot be captured)
   cudaStream_t cap_stream2 = nullptr; // captures the body of the tolerance-mode WHILE node
@@ -378,6 +386,11 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.e_begin = e0; a.e_end = e1;
   a.n_owned = (int32_t)op->sz.n_owned;
   a.halo_mode = 0;
+  if (op->fp_pnew) {  // ASM == 3: x = r_j, xh = p_{j-1}, yh = p_j, idx with designated bits
+    a.idx = op->idx_des.as<int32_t>();
+    a.xh = op->fp_pold;
+    a.yh = op->fp_pnew;
+  }
   if (op->halo_mode_now) {
     a.halo_mode = 1;
     a.xh = op->hx_tab.as<double>();
@@ -1223,6 +1236,67 @@ int finish_result(hb_op* op, int32_t iters, double* rr_hist_host, hb_cg_result* 
   return HB_OK;
 }
 
+// ---- fused-p CG (variant 2, P = 1 fixed mode): iteration j =
+//   operator (ASM == 3): p_j = r_j + beta_j p_{j-1} formed in the gather, stored once per DOF,
+//                        Ap_j accumulated into a zeroed Ap, p_j.Ap_j as element energy
+//   cg_update_xrz:       alpha, x += alpha p_j, r -= alpha Ap_j, Ap = 0, r.r, beta_{j+1}
+// p_j and p_{j-1} alternate between two buffers (the gather of p_{j-1} and the store of p_j
+// overlap in time).  Two kernels per iteration and no grid barrier; 96 N_G + 52 N_L bytes.
+bool fp_eligible(const hb_op* op) {
+  return op->fusedp && op->variant == 2 && !op->comm && op->sz.P == 1 && !op->jacobi && !op->scat_mode;
+}
+
+int fp_iteration(hb_op* op, double* x, int32_t j, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  double* P0 = op->p.as<double>();
+  double* P1 = op->p_alt.as<double>();
+  double* pn = (j & 1) ? P1 : P0;
+  op->fp_pold = (j & 1) ? P0 : P1;
+  op->fp_pnew = pn;
+  const int ls = launch_ax(op, op->ax_fp, 0, op->sz.E_local, op->r.as<double>(), op->Ap.as<double>(), st, true, true);
+  op->fp_pold = nullptr;
+  op->fp_pnew = nullptr;
+  HB_TRY(ls);
+  HB_TRY(phase_event(op, op->t_xr, true, st));
+  double* xp = x;
+  const double* pp = pn;
+  double* rp = op->r.as<double>();
+  double* ap = op->Ap.as<double>();
+  int64_t nn = n;
+  const double* ep = op->e_part.as<double>();
+  int nep = op->last_grid;
+  double* rrp = op->partials.as<double>();
+  hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
+  double* hp = op->hist.as<double>();
+  void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &rrp, &s, &hp};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(op->fused_grid > 0 ? op->fused_grid : vec_grid(std::max<int64_t>(n, 1)));
+  cfg.blockDim = dim3(hbk::VEC_BLOCK);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = op->pdl ? 1 : 0;
+  CU_TRY(cudaLaunchKernelExC(&cfg, (const void*)&hbk::cg_update_xrz, args));
+  op->launches++;
+  HB_TRY(phase_event(op, op->t_xr, false, st));
+  op->last_timed = false;
+  return HB_OK;
+}
+
+int fp_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
+  const int64_t n = op->sz.n_owned;
+  // r = b, p_{-1} = b (any finite value: beta_0 = 0), x = 0, Ap = 0, r.r
+  hbk::cg_init<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
+      b, x, op->r.as<double>(), op->p_alt.as<double>(), op->Ap.as<double>(), n, 0.0, op->partials.as<double>(),
+      op->scal.as<hbk::CgScalars>(), nullptr, nullptr);
+  op->launches++;
+  CU_TRY(cudaGetLastError());
+  CU_TRY(cudaMemsetAsync(&op->scal.as<hbk::CgScalars>()->beta, 0, sizeof(double), st));
+  return HB_OK;
+}
+
 int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_host, hb_cg_result* res,
              cudaStream_t st) {
   HB_TRY(ensure_hist(op, K));
@@ -1240,8 +1314,9 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
     cudaGraph_t graph;
     cudaStream_t cs = op->cap_stream;
     CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int status = cg_init(op, b, x, cs);
-    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
+    const bool fp = fp_eligible(op);
+    int status = fp ? fp_init(op, b, x, cs) : cg_init(op, b, x, cs);
+    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = fp ? fp_iteration(op, x, j, cs) : cg_iteration(op, x, cs);
     cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
     CU_TRY(ce);
@@ -1406,6 +1481,41 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
 
 // CSR of Z^T over owned DOFs, slots in ascending (e, n) order (counting sort by gid), and the
 // y_L buffer -- shared by the deterministic variant and the scattered-storage CG
+// designated slot of every DOF: the first slot (e, n) referencing it
+__global__ void des_first_kernel(const int32_t* __restrict__ idx, int64_t NL, int32_t* first) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < NL; t += (int64_t)gridDim.x * blockDim.x)
+    atomicMin(first + idx[t], (int32_t)t);
+}
+__global__ void des_mark_kernel(const int32_t* __restrict__ idx, int64_t NL, const int32_t* __restrict__ first,
+                                int32_t* out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < NL; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = idx[t];
+    out[t] = first[g] == (int32_t)t ? (int32_t)((uint32_t)g | 0x80000000u) : g;
+  }
+}
+
+static int setup_fusedp(hb_op* op, cudaStream_t st) {
+  if (op->fusedp) return HB_OK;
+  const int64_t NL = op->sz.N_L, n = op->sz.n_owned;
+  if (NL >= INT32_MAX) { set_error("fused-p variant: more than 2^31 slots on one rank"); return HB_ERR_ARG; }
+  HB_TRY(op->idx_des.alloc(NL * 4));
+  HB_TRY(op->p_alt.alloc(std::max<int64_t>(n, 1) * 8));
+  if (NL > 0) {
+    DevBuf first;
+    HB_TRY(first.alloc(n * 4));
+    CU_TRY(cudaMemsetAsync(first.p, 0x7f, n * 4, st));
+    des_first_kernel<<<num_sms() * 8, 256, 0, st>>>(op->idx.as<int32_t>(), NL, first.as<int32_t>());
+    des_mark_kernel<<<num_sms() * 8, 256, 0, st>>>(op->idx.as<int32_t>(), NL, first.as<int32_t>(), op->idx_des.as<int32_t>());
+    CU_TRY(cudaGetLastError());
+    CU_TRY(cudaStreamSynchronize(st));
+  }
+  op->ax_fp = pick_ax(op->N, false, op->mass_mode == 1, 3);
+  HB_TRY(prepare_kernel(op->ax_fp));
+  if ((size_t)op->ax_fp.grid_max * 8 + 64 > op->e_part.bytes) HB_TRY(op->e_part.alloc((size_t)op->ax_fp.grid_max * 8 + 64));
+  op->fusedp = true;
+  return HB_OK;
+}
+
 static int ensure_csr(hb_op* op) {
   if (op->yL.p) return HB_OK;
   const int64_t n = op->sz.n_owned, NL = op->sz.N_L;
@@ -1425,12 +1535,13 @@ static int ensure_csr(hb_op* op) {
 }
 
 extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
-  if (!op || variant < 0 || variant > 1) { set_error("hb_op_set_variant: bad argument"); return HB_ERR_ARG; }
-  if (variant == 1 && (op->sz.P > 1 || op->comm)) {
-    set_error("hb_op_set_variant: the deterministic y_L + CSR variant is available for P = 1 only");
+  if (!op || variant < 0 || variant > 2) { set_error("hb_op_set_variant: bad argument"); return HB_ERR_ARG; }
+  if (variant >= 1 && (op->sz.P > 1 || op->comm)) {
+    set_error("hb_op_set_variant: variants 1 and 2 are available for P = 1 only");
     return HB_ERR_STATE;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (variant == 2) HB_TRY(setup_fusedp(op, st));
   if (variant == 1) {
     HB_TRY(ensure_csr(op));
     if (!op->ax_yl.fn) {

@@ -344,7 +344,8 @@ class Operator:
         return res.iterations, (h[:res.iterations + 1].copy() if hist else None)
 
     def set_variant(self, variant: int, stream=None):
-        """0: fused scatter-add (default); 1: y_L + deterministic CSR gather (P = 1)."""
+        """0: fused scatter-add (default); 1: y_L + deterministic CSR gather (P = 1);
+        2: fused p update -- the CG p update runs inside the next operator (P = 1, fixed mode)."""
         _check(_lib.hb_op_set_variant(self._h, int(variant), _stream(stream)))
 
     def set_jacobi(self, enable: bool, stream=None):

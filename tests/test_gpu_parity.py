@@ -518,3 +518,42 @@ def test_scattered_storage_cg(hb, box, N):
     _cg_contract(hf, ho, jo - 1)
     with pytest.raises(hb.HBError, match="STATE"):
         hb.Operator(hb.Mesh(*box, N, mass_mode=1)).cg_scattered(b, x, 3)
+
+
+@pytest.mark.parametrize("box,N,mass_mode", [((3, 3, 2), 3, 0), ((4, 3, 3), 7, 1), ((16, 16, 16), 7, 0),
+                                             ((3, 2, 2), 12, 0), ((5, 2, 3), 1, 0)])
+def test_fused_p_variant_cg(hb, box, N, mass_mode):
+    """Variant 2 (fused p update: p_j = r_j + beta_j p_{j-1} formed in the operator's gather
+    and stored once per DOF by its designated slot, Ap zero-initialised, lambda W added once
+    per DOF): fixed-mode CG against the oracle's Alg. 1 (c18), random SPD geometry; operator
+    applies and tolerance mode (which keep the standard path) still agree."""
+    E = int(np.prod(box))
+    xg, w = basis.gll(N)
+    wq = np.einsum("k,j,i->kji", w, w, w).ravel()
+    G = random_spd_factors(E, (N + 1) ** 3, seed=71 + N, scale=wq)
+    B = random_positive((E, (N + 1) ** 3), 5) if mass_mode == 1 else None
+    o = OracleProblem(box, N, mass_mode=mass_mode, G=G, B=B)
+    m = hb.Mesh(*box, N, mass_mode=mass_mode)
+    m.set_geometry(G)
+    if B is not None:
+        m.set_mass(B)
+    op = hb.Operator(m)
+    op.set_variant(2)
+    A = lambda v: o.apply(v, 1.0)
+    bo = of.forcing(range(o.NG), 1)
+    K = 40
+    xo, _, ho = ocg.cg(A, bo, max_iters=K)
+    jt = min(K, next((k for k, v in enumerate(ho) if v <= 1e-16 * ho[0]), K))
+    b = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.forcing(1, b)
+    for rep in range(2):  # second solve replays the captured graph
+        x = torch.zeros_like(b)
+        j, h = op.cg(b, x, K)
+        assert j == K
+        _cg_contract(h, ho, jt - 1)
+        if jt == K:
+            assert np.abs(x.cpu().numpy() - xo).max() <= 1e-10 * np.abs(xo).max()
+    xv = uniform_vector(o.NG, 13)
+    y = torch.empty(o.NG, dtype=torch.float64, device="cuda")
+    op.apply(dev(xv), y)
+    assert (np.abs(y.cpu().numpy() - A(xv)) / o.scale(xv, 1.0)).max() <= 1e-12
