@@ -121,6 +121,12 @@ def test_error_paths(hb):
         hb.Mesh(2, 2, 2, 3, mass_mode=0).set_mass(np.ones(8 * 64))
     with pytest.raises(hb.HBError, match="HB_ERR_ARG"):
         hb.gll(0)
+    # IPC communicator: argument checks happen before any CUDA call
+    for P, r in ((0, 0), (2, 2), (2, -1), (33, 0)):
+        with pytest.raises(hb.HBError, match="HB_ERR_ARG"):
+            hb.Comm.create_ipc(P, r)
+    c = hb.Comm.create_ipc(1, 0)  # P = 1: valid, needs no driver entry points
+    assert c.ipc
 
 
 def test_set_geometry_roundtrip(hb):
