@@ -29,6 +29,13 @@ def nccl_root() -> str:
 SOURCES = ["mesh.cpp", "op.cu"]
 
 
+def _stamp_name() -> str:
+    """Build flavour of the library on disk (plain, or a tuning build for one / all degrees)."""
+    if not os.environ.get("HB_TUNE"):
+        return ".plain"
+    return ".tune" + (f"_n{int(os.environ['HB_TUNE_N'])}" if os.environ.get("HB_TUNE_N") else "")
+
+
 def _compile(src: str, nccl: str, extra: list[str]) -> str:
     obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
     cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3",
@@ -52,7 +59,7 @@ def build(force: bool = False, extra: list[str] | None = None) -> str:
     hdrs.append(os.path.join(ROOT, "include", "hipbone_b200.h"))
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
-        stamp = os.path.join(LIBDIR, ".tune" if os.environ.get("HB_TUNE") else ".plain")
+        stamp = os.path.join(LIBDIR, _stamp_name())
         if all(os.path.getmtime(f) < t for f in srcs + hdrs + [__file__]) and os.path.exists(stamp):
             return LIB
     nccl = nccl_root()
@@ -65,10 +72,10 @@ def build(force: bool = False, extra: list[str] | None = None) -> str:
         raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     for o in objs:
         os.remove(o)
-    for st in (".tune", ".plain"):
-        if os.path.exists(os.path.join(LIBDIR, st)):
+    for st in os.listdir(LIBDIR):
+        if st.startswith((".tune", ".plain")):
             os.remove(os.path.join(LIBDIR, st))
-    open(os.path.join(LIBDIR, ".tune" if os.environ.get("HB_TUNE") else ".plain"), "w").close()
+    open(os.path.join(LIBDIR, _stamp_name()), "w").close()
     return LIB
 
 

@@ -46,7 +46,7 @@ struct LinesShape {
   // Shared-memory layout of one element buffer: (i,j,k) -> doubles.  NP = 8 and NP = 16 use an
   // XOR swizzle that makes all three line orientations conflict free; other N use row / layer
   // padding from an offline bank-conflict search.
-  static constexpr int PAD[16][3] = {{0, 0, 0},       {2, 5, 12},      {3, 9, 27},       {4, 19, 76},
+  static constexpr int PAD[16][3] = {{0, 0, 0},       {2, 5, 12},      {3, 12, 42},      {4, 19, 76},
                                      {5, 25, 125},    {9, 54, 324},    {7, 52, 369},     {8, 72, 576},
                                      {9, 81, 729},    {10, 101, 1010}, {11, 121, 1331},  {13, 156, 1872},
                                      {13, 169, 2197}, {17, 238, 3332}, {15, 225, 3375},  {16, 256, 4096}};
