@@ -268,6 +268,7 @@ struct hb_op {
   bool scat_mode = false;  // operator launches read x_L (sL_p) and write y_L
   DevBuf sL_x, sL_r, sL_p, sL_w, sW;
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
+  const void* fused_fn = nullptr;  // cg_update_fused<U> instance (U double2 per thread per batch)
   bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
   std::vector<int32_t> nbr;
@@ -871,7 +872,21 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     int dev = 0, coop = 0, nb = 0;
     CU_TRY(cudaGetDevice(&dev));
     CU_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)&hbk::cg_update_fused, hbk::VEC_BLOCK, 0));
+    const char* ue = getenv("HB_UPD_U");
+    const char* me = getenv("HB_UPD_MINB");
+    // default: the batched form (first batch in flight during the p.Ap reduction) for vectors that
+    // fit L2 (C2: +1.3%), the single-item form above that (C3 N=7: the batched one is 2.7% slower;
+    // profiles/r1_update_ab.jsonl)
+    const int U = ue ? atoi(ue) : (n <= 8000000 ? 1 : 0), MB = me ? atoi(me) : 2;
+    if (U == 0)
+      op->fused_fn = (const void*)&hbk::cg_update_fused0;
+    else if (MB >= 2)
+      op->fused_fn = U >= 4 ? (const void*)&hbk::cg_update_fused<4, 2>
+                   : U == 2 ? (const void*)&hbk::cg_update_fused<2, 2> : (const void*)&hbk::cg_update_fused<1, 2>;
+    else
+      op->fused_fn = U >= 4 ? (const void*)&hbk::cg_update_fused<4, 1>
+                   : U == 2 ? (const void*)&hbk::cg_update_fused<2, 1> : (const void*)&hbk::cg_update_fused<1, 1>;
+    CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, op->fused_fn, hbk::VEC_BLOCK, 0));
     const char* env = getenv("HB_FUSED_UPDATE");
     if (coop && nb > 0 && !(env && env[0] == '0'))
       op->fused_grid = std::min(vec_grid(std::max<int64_t>(n, 1)), nb * num_sms());
@@ -1148,7 +1163,7 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = op->pdl ? 2 : 1;
-    CU_TRY(cudaLaunchKernelExC(&cfg, (const void*)&hbk::cg_update_fused, args));
+    CU_TRY(cudaLaunchKernelExC(&cfg, op->fused_fn, args));
     op->launches++;
     return phase_event(op, op->t_xr, false, st);
   }

@@ -182,8 +182,9 @@ cg_update_xr_e(double* __restrict__ x, const double* __restrict__ p, double* __r
 // sums the r.r partials in CTA order -> beta; p = r + beta p, Ap = lambda p, CTA partial of
 // p.p (consumed by the next iteration's p.Ap).  r and p are re-read after the barrier from L2
 // when the vectors fit it.  CTA 0 publishes the scalars (pAp, rr, rr_new, history, j).
+// (previous single-item form, kept for A/B: HB_UPD_U=0)
 __global__ void __launch_bounds__(VEC_BLOCK)
-cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
+cg_update_fused0(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
                 double lam_init, double* rr_part, CgScalars* s, double* hist, const double* __restrict__ invd,
                 double* rz_part) {
@@ -277,6 +278,152 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       p[l] = pv; Ap[l] = lam_init * pv;
       acc2 = fma(pv, pv, acc2);
     }
+  }
+  acc2 = block_sum(acc2);
+  if (threadIdx.x == 0) {
+    pp_part[blockIdx.x] = acc2;  // every CTA read the old partials before the grid barrier
+    if (blockIdx.x == 0) {
+      s->pAp = pAp;
+      s->rr = rr;
+      if (hist) hist[s->it] = rr;
+      s->rr_new = rr_new;
+      s->rz = rho_new;
+      s->it += 1;
+    }
+  }
+}
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(VEC_BLOCK, MINB)
+cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
+                int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
+                double lam_init, double* rr_part, CgScalars* s, double* hist, const double* __restrict__ invd,
+                double* rz_part) {
+  // U double2 per thread per batch: every load of a batch is issued before any use, and the
+  // first batch is in flight while the CTA reduces the p.Ap partials.  When a thread's whole
+  // share fits one batch, the p update reuses the registers (r_{j+1}, p_j, M^-1) -- no re-read.
+  __shared__ double s_b[3];
+  pdl_wait();
+  const int64_t n2 = n >> 1;
+  const int64_t stride = (int64_t)gridDim.x * VEC_BLOCK;
+  const int64_t tid = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x;
+  const bool one = n2 <= (int64_t)U * stride;  // grid-uniform
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  double2* a2 = reinterpret_cast<double2*>(Ap);
+  const double2* d2 = reinterpret_cast<const double2*>(invd);
+  double2 xv[U], pv[U], rv[U], av[U], dv[U];
+  auto load1 = [&](int64_t l0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t l = l0 + u * stride;
+      if (l < n2) {
+        xv[u] = x2[l]; pv[u] = p2[l]; rv[u] = r2[l]; av[u] = a2[l];
+        if (invd) dv[u] = d2[l];
+      }
+    }
+  };
+  if (tid < n2) load1(tid);
+  // ---- p.Ap and alpha (identical in every CTA)
+  double ev = 0.0, pv_ = 0.0;
+  for (int b = threadIdx.x; b < n_epart; b += VEC_BLOCK) ev += e_part[b];
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) pv_ += pp_part[b];
+  ev = block_sum(ev);
+  __syncthreads();
+  pv_ = block_sum(pv_);
+  const double rr = s->rr_new;             // r_j.r_j
+  const double rho = invd ? s->rz : rr;     // r_j.z_j (PCG) or r_j.r_j (CG)
+  if (threadIdx.x == 0) s_b[0] = ev + lam_pp * pv_;
+  __syncthreads();
+  const double pAp = s_b[0];
+  const double alpha = (pAp != 0.0) ? rho / pAp : 0.0;  // c15 guard
+  // ---- x, r update + r.r (+ r.z)
+  double acc = 0.0, acc_rz = 0.0;
+  for (int64_t l0 = tid; l0 < n2;) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t l = l0 + u * stride;
+      if (l < n2) {
+        xv[u].x = fma(alpha, pv[u].x, xv[u].x); xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+        rv[u].x = fma(-alpha, av[u].x, rv[u].x); rv[u].y = fma(-alpha, av[u].y, rv[u].y);
+        x2[l] = xv[u]; r2[l] = rv[u];
+        acc = fma(rv[u].x, rv[u].x, acc); acc = fma(rv[u].y, rv[u].y, acc);
+        if (invd) {
+          acc_rz = fma(rv[u].x, rv[u].x * dv[u].x, acc_rz); acc_rz = fma(rv[u].y, rv[u].y * dv[u].y, acc_rz);
+        }
+      }
+    }
+    l0 += (int64_t)U * stride;
+    if (l0 < n2) load1(l0);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    x[l] = fma(alpha, p[l], x[l]);
+    const double rvl = fma(-alpha, Ap[l], r[l]);
+    r[l] = rvl;
+    acc = fma(rvl, rvl, acc);
+    if (invd) acc_rz = fma(rvl, rvl * invd[l], acc_rz);
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) rr_part[blockIdx.x] = acc;
+  if (invd) {
+    __syncthreads();
+    acc_rz = block_sum(acc_rz);
+    if (threadIdx.x == 0) rz_part[blockIdx.x] = acc_rz;
+  }
+  cooperative_groups::this_grid().sync();
+  // ---- beta (identical in every CTA), p update + p.p
+  double rn = 0.0, zn = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) rn += __ldcg(rr_part + b);
+  rn = block_sum(rn);
+  if (threadIdx.x == 0) s_b[1] = rn;
+  if (invd) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += VEC_BLOCK) zn += __ldcg(rz_part + b);
+    zn = block_sum(zn);
+    if (threadIdx.x == 0) s_b[2] = zn;
+  }
+  __syncthreads();
+  const double rr_new = s_b[1];
+  const double rho_new = invd ? s_b[2] : rr_new;
+  const double beta = (rho != 0.0) ? rho_new / rho : 0.0;  // c15 guard
+  double acc2 = 0.0;
+  auto pupd = [&](int64_t l, double2 pvv, double2 rvv, double2 dvv) {
+    if (invd) { rvv.x *= dvv.x; rvv.y *= dvv.y; }  // z = M^-1 r
+    pvv.x = fma(beta, pvv.x, rvv.x); pvv.y = fma(beta, pvv.y, rvv.y);
+    p2[l] = pvv;
+    a2[l] = make_double2(lam_init * pvv.x, lam_init * pvv.y);
+    acc2 = fma(pvv.x, pvv.x, acc2); acc2 = fma(pvv.y, pvv.y, acc2);
+  };
+  if (one) {  // this thread's r_{j+1}, p_j (and M^-1) are still in registers
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t l = tid + u * stride;
+      if (l < n2) pupd(l, pv[u], rv[u], invd ? dv[u] : make_double2(0.0, 0.0));
+    }
+  } else {
+    for (int64_t l0 = tid; l0 < n2; l0 += (int64_t)U * stride) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t l = l0 + u * stride;
+        if (l < n2) {
+          pv[u] = p2[l]; rv[u] = __ldcg(r2 + l);
+          if (invd) dv[u] = d2[l];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t l = l0 + u * stride;
+        if (l < n2) pupd(l, pv[u], rv[u], invd ? dv[u] : make_double2(0.0, 0.0));
+      }
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t l = n - 1;
+    const double pvl = fma(beta, p[l], __ldcg(r + l) * (invd ? invd[l] : 1.0));
+    p[l] = pvl; Ap[l] = lam_init * pvl;
+    acc2 = fma(pvl, pvl, acc2);
   }
   acc2 = block_sum(acc2);
   if (threadIdx.x == 0) {
