@@ -337,13 +337,29 @@ def main():
                 pj = json.load(f)
             key = f"N{N}_{blk[0]}x{blk[1]}x{blk[2]}"
             traffic = pj.get("dram_bytes_per_launch", {}).get(key)
+        s81 = None  # the paper's 8:1 streaming rate, measured on a B200 by scripts/calib.py
+        cal = os.path.join(ROOT, "profiles", "r1_calib_stream8to1.json")
+        if os.path.exists(cal):
+            with open(cal) as f:
+                s81 = json.load(f).get("asymptotic_GBps")
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac_of_datasheet_7700": round(achieved / 7700.0, 4),
+                "frac_of_stream8to1": round(achieved / s81, 4) if s81 else None,
                 "kernel": f"ax_lines<N={N}>" + (" (A + halo + B launches of one apply, summed)" if world > 1 else ""),
                 "launch_ms": round(mean_s * 1e3, 4), "launches_timed": n_l,
                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                 "paper_ledger_gbs": round(ledger.op_bytes_paper(n, NL_loc) / mean_s / 1e9, 1),
                 "op_gflops": round(ledger.op_flops(s["E_local"], N) / mean_s / 1e9, 1)}
+
+    measured_bpd = None
+    prof = os.path.join(ROOT, "profiles", "ncu_op_summary.json")
+    if world == 1 and args.variant == 0 and args.storage == "assembled" and os.path.exists(prof):
+        with open(prof) as f:
+            dbl = json.load(f).get("dram_bytes_per_launch", {})
+        ko, kv = f"N{N}_{blk[0]}x{blk[1]}x{blk[2]}", f"vec_N{N}_{blk[0]}x{blk[1]}x{blk[2]}"
+        if ko in dbl and kv in dbl:
+            measured_bpd = round((dbl[ko] + dbl[kv]) / NG, 2)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -371,6 +387,9 @@ def main():
                # assembled-storage minimum 108 + 80 N_L/N_G
                "bytes_per_dof_iter": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) / NG, 2),
                "bytes_per_dof_iter_paper": round(ledger.cg_bytes_paper(NG, E_glob * (N + 1) ** 3) / NG, 2),
+               # ncu DRAM bytes of one iteration's kernels (operator + vector update, committed
+               # capture of this workload) per DOF
+               "bytes_per_dof_iter_measured": measured_bpd,
                "cg_gbs_fused_ledger": round(ledger.cg_bytes_fused(NG, E_glob * (N + 1) ** 3) * K / (ms * 1e-3) / 1e9, 1),
                "e2e": ({"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
                         "d2h_bytes_per_step": 8 * n + 48} if e2e_ms else None),

@@ -28,7 +28,9 @@ for s in $STAGES; do
          timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ax_lines -s 5 -c 1 -o $O/prof_ax_c3 -f \
            python scripts/opbench.py --N 7 --box 52,52,52 --reps 3 > $O/ncu_full3.log 2>&1; echo "ncu-full3 rc=$?" >> $O/status.txt ;;
     ncuvec) timeout 1200 ncu --set full --clock-control none -k regex:cg_update -s 10 -c 1 -o $O/prof_vec_c2 -f \
-           python bench.py --steps 1 --warmup 1 --iters 5 --no-cpu-baseline --no-profile > $O/ncu_vec.log 2>&1; echo "ncu-vec rc=$?" >> $O/status.txt ;;
+           python bench.py --steps 1 --warmup 1 --iters 5 --no-cpu-baseline --no-profile > $O/ncu_vec.log 2>&1; echo "ncu-vec rc=$?" >> $O/status.txt
+            timeout 1200 ncu --set full --clock-control none -k regex:cg_update -s 10 -c 1 -o $O/prof_vec_c3 -f \
+           python bench.py --box 52,52,52 --steps 1 --warmup 1 --iters 5 --no-cpu-baseline --no-profile > $O/ncu_vec3.log 2>&1; echo "ncu-vec3 rc=$?" >> $O/status.txt ;;
     calib) timeout 300 python scripts/calib.py > $O/calib.json 2>> $O/calib.err; echo "calib rc=$?" >> $O/status.txt ;;
   esac
 done
