@@ -1,0 +1,131 @@
+// Fused screened-Poisson operator for N = 1 (trilinear hexahedra): one element per thread.
+//
+// Same operation as ax_lines.cuh (P:94-108, P:154 with Z^T fused), specialised for the
+// degree where every node is an element vertex: the whole element (8 values, 24 gradient
+// components, 48 geometric factors) lives in one thread's registers, so the three
+// contractions need no shared-memory transposes or barriers.  The only shared-memory use is
+// to turn the G stream coalesced: a CTA's elements are consecutive, so their G slabs form one
+// contiguous block that the CTA copies with 16-byte streaming loads into shared memory,
+// padded to 49 doubles per element so that each thread's reads of its own 48 factors hit 16
+// distinct bank pairs per half-warp.  All eight nodes are shared with neighbours (no
+// element-interior node at N = 1): every output is an fp64 RED into Ap, pre-initialised to
+// lambda p by the CG p update (reading R2), or into the halo accumulator.
+#pragma once
+#include <cstdint>
+
+#include "ax_lines.cuh"  // energy_finish, AxArgs, load_x / red_y
+
+namespace hbk {
+
+template <int EPB>
+struct VertexShape {
+  static constexpr int BLOCK = EPB;               // one element per thread
+  static constexpr int GPAD = 49;                 // doubles per element in shared memory
+  static constexpr size_t SMEM = sizeof(double) * (size_t)EPB * GPAD;
+};
+
+template <int EPB, bool HALO, bool MASSB, int MINB, int PFB = 1>
+__global__ void __launch_bounds__(EPB, MINB)
+ax_vertex(const AxArgs a) {
+  constexpr int N = 1, NP = 2, NP2 = 4, NP3 = 8, GE = 6 * NP3;  // 48 factors per element
+  using S = VertexShape<EPB>;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x;
+  // D of degree 1 from constant memory (uniform): D[i][m] = c_D[1][i*2+m]
+  double D[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) D[i][m] = c_D[N][i * NP + m];
+  double en = 0.0;
+
+  for (int64_t base = a.e_begin + (int64_t)blockIdx.x * EPB; base < a.e_end; base += (int64_t)gridDim.x * EPB) {
+    const int64_t ne = (a.e_end - base) < EPB ? (a.e_end - base) : EPB;
+    const int64_t e = base + t;
+    const bool act = t < ne;
+    if constexpr (PFB > 0) {  // L2 prefetch of G PFB batches ahead (one 128-byte line per thread-slot)
+      const int64_t nb = base + (int64_t)PFB * gridDim.x * EPB;
+      if (nb < a.e_end) {
+        const int64_t nn = (a.e_end - nb) < EPB ? (a.e_end - nb) : EPB;
+        const char* gb = reinterpret_cast<const char*>(a.G + nb * GE);
+        for (int q = t; q < (int)(nn * GE * 8 / 128); q += EPB) prefetch_l2_line(gb + q * 128);
+      }
+    }
+    // ---- gather (Z x): the element's 8 indices are 32 contiguous bytes
+    int32_t gi[NP3];
+    double u[NP3];
+    if (act) {
+      const int4* ip = reinterpret_cast<const int4*>(a.idx + e * NP3);
+      const int4 i0 = __ldg(ip), i1 = __ldg(ip + 1);
+      gi[0] = i0.x; gi[1] = i0.y; gi[2] = i0.z; gi[3] = i0.w;
+      gi[4] = i1.x; gi[5] = i1.y; gi[6] = i1.z; gi[7] = i1.w;
+#pragma unroll
+      for (int n = 0; n < NP3; ++n) u[n] = load_x<HALO>(a, gi[n]);
+    } else {
+#pragma unroll
+      for (int n = 0; n < NP3; ++n) { gi[n] = 0; u[n] = 0.0; }
+    }
+    // ---- G of the CTA's elements: one contiguous block, coalesced 16-byte streaming loads
+    {
+      const double2* g2 = reinterpret_cast<const double2*>(a.G + base * GE);
+      const int nd2 = (int)ne * (GE / 2);
+      for (int q = t; q < nd2; q += EPB) {
+        const double2 v = __ldcs(g2 + q);
+        const int d = 2 * q, el = d / GE, f = d - el * GE;
+        smem[el * S::GPAD + f] = v.x;
+        smem[el * S::GPAD + f + 1] = v.y;
+      }
+    }
+    __syncthreads();
+    if (act) {
+      // ---- gradients: node n = i + 2 j + 4 k
+      double ur[NP3], us[NP3], ut[NP3];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int n = i + 2 * j + 4 * k;
+            ur[n] = D[i][0] * u[0 + 2 * j + 4 * k] + D[i][1] * u[1 + 2 * j + 4 * k];
+            us[n] = D[j][0] * u[i + 0 + 4 * k] + D[j][1] * u[i + 2 + 4 * k];
+            ut[n] = D[k][0] * u[i + 2 * j + 0] + D[k][1] * u[i + 2 * j + 4];
+          }
+      // ---- metric: G slab layout [k][factor][(j,i)]
+      const double* gs = smem + t * S::GPAD;
+      double vr[NP3], vs[NP3], vt[NP3];
+#pragma unroll
+      for (int n = 0; n < NP3; ++n) {
+        const int k = n >> 2, c = n & 3;
+        const double* g = gs + k * 6 * NP2 + c;
+        const double grr = g[0], grs = g[NP2], grt = g[2 * NP2], gss = g[3 * NP2], gst = g[4 * NP2], gtt = g[5 * NP2];
+        vr[n] = grr * ur[n] + grs * us[n] + grt * ut[n];
+        vs[n] = grs * ur[n] + gss * us[n] + gst * ut[n];
+        vt[n] = grt * ur[n] + gst * us[n] + gtt * ut[n];
+      }
+      // ---- divergence (transposed contractions) and assembly Z^T
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int n = i + 2 * j + 4 * k;
+            double out = D[0][i] * vr[0 + 2 * j + 4 * k] + D[1][i] * vr[1 + 2 * j + 4 * k]
+                       + D[0][j] * vs[i + 0 + 4 * k] + D[1][j] * vs[i + 2 + 4 * k]
+                       + D[0][k] * vt[i + 2 * j + 0] + D[1][k] * vt[i + 2 * j + 4];
+            en = fma(u[n], out, en);
+            if (MASSB) {
+              const double lb = a.lam * __ldg(a.B + e * NP3 + n) * u[n];
+              out += lb;
+              en = fma(u[n], lb, en);
+            }
+            red_y<HALO>(a, gi[n], out);
+          }
+    }
+    __syncthreads();  // the next batch overwrites the G block
+  }
+  if (a.cg) energy_finish<EPB>(en, a, smem);
+}
+
+}  // namespace hbk

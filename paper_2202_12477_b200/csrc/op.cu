@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "ax_lines.cuh"
+#include "ax_vertex.cuh"
 #include "internal.h"
 #include "vec.cuh"
 
@@ -101,6 +102,32 @@ AxKernel make_lines() {
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
   return k;
+}
+
+template <int EPB, bool HALO, bool MASSB, int MINB, int PFB = 1>
+AxKernel make_vertex() {
+  AxKernel k;
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_vertex<EPB, HALO, MASSB, MINB, PFB>);
+  k.block = hbk::VertexShape<EPB>::BLOCK;
+  k.epb = EPB;
+  k.smem = hbk::VertexShape<EPB>::SMEM;
+  return k;
+}
+
+// N = 1, fused scatter-add: one element per thread (ax_vertex.cuh), 64 elements per CTA
+// with an L2 prefetch of G one grid batch ahead (C3: 3.86 ms = 0.86 of peak; no prefetch
+// 4.59 ms, line kernel 5.56 ms); env HB_N1_LINES=1, HB_N1_EPB=32|64|128, HB_N1_PF=0|1|2 for A/B
+AxKernel pick_vertex(bool halo, bool massb) {
+  const char* ev = getenv("HB_N1_EPB");
+  const char* pv = getenv("HB_N1_PF");
+  const int epb = ev ? atoi(ev) : 64, pf = pv ? atoi(pv) : 1;
+#define HB_VX(E, M, P) \
+  (halo ? (massb ? make_vertex<E, true, true, M, P>() : make_vertex<E, true, false, M, P>()) \
+        : (massb ? make_vertex<E, false, true, M, P>() : make_vertex<E, false, false, M, P>()))
+  if (epb == 32) return pf == 0 ? HB_VX(32, 16, 0) : pf == 2 ? HB_VX(32, 16, 2) : HB_VX(32, 16, 1);
+  if (epb == 128) return pf == 0 ? HB_VX(128, 4, 0) : pf == 2 ? HB_VX(128, 4, 2) : HB_VX(128, 4, 1);
+  return pf == 0 ? HB_VX(64, 8, 0) : pf == 2 ? HB_VX(64, 8, 2) : HB_VX(64, 8, 1);
+#undef HB_VX
 }
 
 constexpr int kLinesPF = 0;  // L2 bulk prefetch distance (grid waves); measured slower on B200
@@ -183,6 +210,10 @@ AxKernel pick_ax(int N, bool halo, bool massb, int asm_mode = 0) {
     if (v && atoi(v) > 0 && vn && atoi(vn) == N) return pick_ax_variant(N, atoi(v));
   }
 #endif
+  if (N == 1 && asm_mode == 0) {
+    const char* l = getenv("HB_N1_LINES");
+    if (!(l && l[0] == '1')) return pick_vertex(halo, massb);
+  }
   switch (N) {
     case 1: return pick_ax_n<1>(halo, massb, asm_mode);
     case 2: return pick_ax_n<2>(halo, massb, asm_mode);

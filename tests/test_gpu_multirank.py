@@ -26,7 +26,7 @@ def _run(P, box, N, port):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("P,box,N,port", [(2, (4, 3, 4), 3, 29611), (4, (5, 4, 3), 2, 29612),
-                                           (3, (6, 2, 2), 5, 29613)])
+                                           (3, (6, 2, 2), 5, 29613), (2, (7, 5, 3), 1, 29614)])
 def test_ipc_transport_parity(P, box, N, port):
     out = _run(P, box, N, port)
     assert "error" not in out, out

@@ -262,7 +262,7 @@ def test_loopback_group_apply_and_cg(hb, P):
     assert np.abs(x - xo).max() <= 1e-10 * np.abs(xo).max()
 
 
-@pytest.mark.parametrize("box,N", [((52, 52, 52), 7), ((24, 24, 24), 15), ((122, 122, 122), 3)])
+@pytest.mark.parametrize("box,N", [((52, 52, 52), 7), ((24, 24, 24), 15), ((122, 122, 122), 3), ((120, 100, 91), 1)])
 def test_full_size_C3_sampled_and_properties(hb, box, N):
     """C3 at full size (~50 M DOFs), the launch configuration bench.py / opbench time:
     sampled entries against the oracle computed one by one (c17 scale from |D|, |G|), plus
@@ -345,7 +345,7 @@ def test_cg_random_geometry_both_mass_modes(hb, N, mass_mode):
     _cg_contract(hf, ho, jo - 1)
 
 
-@pytest.mark.parametrize("box,N,P", [((5, 4, 3), 7, 4), ((6, 3, 5), 2, 6), ((3, 3, 3), 5, 3)])
+@pytest.mark.parametrize("box,N,P", [((5, 4, 3), 7, 4), ((6, 3, 5), 2, 6), ((3, 3, 3), 5, 3), ((9, 7, 5), 1, 4)])
 def test_loopback_uneven_partitions_cg(hb, box, N, P):
     """Uneven element splits (remainder layers), several neighbour counts, N=2..7: the split
     apply with per-rank compute/communication streams and the loopback transport (the NCCL
