@@ -94,14 +94,29 @@ struct AxKernel {
 };
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0,
-          bool PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false>
+          bool PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false, bool PIPE = false, bool GSM = false, int STRM = -1>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN, PIPE, GSM, STRM>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
-  k.smem = hbk::LinesShape<N, EPBX>::SMEM;
+  k.smem = PIPE ? hbk::LinesShape<N, EPBX>::SMEM_PIPE
+                : (GSM ? hbk::LinesShape<N, EPBX>::SMEM_GSM : hbk::LinesShape<N, EPBX>::SMEM);
   return k;
+}
+
+// Asynchronous-gather operator (PIPE, ax_lines.cuh) for the fused owned-only apply: env
+// HB_AX_PIPE = comma list of degrees (or "all"), HB_AX_PIPE_PFN=1 prefetches G one element ahead
+bool deg_listed(const char* var, int N) {
+  const char* v = getenv(var);
+  if (!v) return false;
+  if (!strcmp(v, "all")) return true;
+  for (const char* q = v; *q;) {
+    if (atoi(q) == N) return true;
+    while (*q && *q != ',') ++q;
+    if (*q == ',') ++q;
+  }
+  return false;
 }
 
 template <int EPB, bool HALO, bool MASSB, int MINB, int PFB = 1>
@@ -144,6 +159,34 @@ AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
   if (asm_mode == 3)
     return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 3>()
                  : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 3>();
+  if constexpr (N >= 2 && N <= 5) {
+    if (deg_listed("HB_AX_GSM", N)) {
+      constexpr int MG = hbk::LinesShape<N>::MINB_GSM;
+      return massb ? make_lines<N, false, true, kLinesPF, MG, 0, false, true, 0, false, false, true>()
+                   : make_lines<N, false, false, kLinesPF, MG, 0, false, true, 0, false, false, true>();
+    }
+  }
+  if (!massb && N >= 8 && deg_listed("HB_AX_STREAM", N)) {
+    // experiment: streaming line contractions (as N = 12) at other degrees; HB_AX_STREAM_MINB=1
+    // uncaps the registers (one CTA per SM), HB_AX_PIPE adds the asynchronous gather
+    constexpr int M = hbk::LinesShape<N>::MINB;
+    const char* mb = getenv("HB_AX_STREAM_MINB");
+    const bool one = mb && mb[0] == '1';
+    if (deg_listed("HB_AX_PIPE", N))
+      return one ? make_lines<N, false, false, kLinesPF, 1, 0, PL, true, 0, false, true, false, 1>()
+                 : make_lines<N, false, false, kLinesPF, hbk::LinesShape<N>::MINB_PIPE, 0, PL, true, 0, false, true, false, 1>();
+    return one ? make_lines<N, false, false, kLinesPF, 1, 0, PL, true, 0, false, false, false, 1>()
+               : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 0, false, false, false, 1>();
+  }
+  if (deg_listed("HB_AX_PIPE", N)) {
+    constexpr int MP = hbk::LinesShape<N>::MINB_PIPE;
+    const char* pfn = getenv("HB_AX_PIPE_PFN");
+    if (pfn && pfn[0] == '1')
+      return massb ? make_lines<N, false, true, kLinesPF, MP, 0, true, true, 0, true, true>()
+                   : make_lines<N, false, false, kLinesPF, MP, 0, true, true, 0, true, true>();
+    return massb ? make_lines<N, false, true, kLinesPF, MP, 0, PL, true, 0, false, true>()
+                 : make_lines<N, false, false, kLinesPF, MP, 0, PL, true, 0, false, true>();
+  }
   return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
 }
 
