@@ -332,7 +332,7 @@ def main():
         roof_apply_s = mean_s
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_op_summary.json")
-        if os.path.exists(prof):
+        if world == 1 and os.path.exists(prof):  # captures are single-GPU launches of this workload
             with open(prof) as f:
                 pj = json.load(f)
             key = f"N{N}_{blk[0]}x{blk[1]}x{blk[2]}"

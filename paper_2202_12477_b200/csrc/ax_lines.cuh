@@ -66,10 +66,6 @@ struct LinesShape {
   static constexpr int CONST = 2 * MAT;               // D and D^T (host-built, g_EO[N])
   static_assert(CONST <= EO_MAX, "folded D table");
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
-  // PIPE: u ping-pong (2 buffers) + r, s + the index blocks of the current and next element
-  // GSM: + the CTA's element group of G (one contiguous 48 NP3 EPB-byte range) and an mbarrier
-  static constexpr size_t SMEM_GSM = SMEM + 48 * NP3 * EPB + 16;
-  static constexpr size_t SMEM_PIPE = sizeof(double) * (4 * EPB * SLAB + CONST) + sizeof(int32_t) * 2 * EPB * NP3;
   // Resident CTAs per SM requested from ptxas, from a per-N register target measured on the
   // B200 (profiles/r1_tune.jsonl; 0 = no cap, one CTA per SM), capped by shared memory.
   // N = 12: streaming line contractions (no output arrays) fit 2 CTAs/SM without spills
@@ -82,12 +78,12 @@ struct LinesShape {
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
   static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = MINB_REG < MINB_SMEM ? MINB_REG : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
-  static constexpr int MINB_SMEM_P = (int)((227 * 1024) / (SMEM_PIPE + 1024));
-  static constexpr int MINB_SMEM_G = (int)((227 * 1024) / (SMEM_GSM + 1024));
-  static constexpr int MINB_GSM = MINB_REG < MINB_SMEM_G ? MINB_REG : (MINB_SMEM_G < 1 ? 1 : MINB_SMEM_G);
-  static constexpr int MINB_PIPE = MINB_REG < MINB_SMEM_P ? MINB_REG : (MINB_SMEM_P < 1 ? 1 : MINB_SMEM_P);
-  // per-element L2 prefetch of G: a gain from N = 6 up, a 1-3% loss below (profiles/r1_tune2.jsonl)
-  static constexpr bool PFL_DEF = N >= 6;
+  // per-element L2 prefetch of G: a gain from N = 6 up, a 1-3% loss below (profiles/r1_tune2.jsonl).
+  // 1 = one prefetch.global.L2 per 128-byte line by the element's threads, 2 = one bulk
+  // prefetch (cp.async.bulk.prefetch.L2) of the element's whole G range by one thread: fewer
+  // LSU instructions, +4..14% at N = 8, 11-15, -5% at N = 7, 10 (profiles/r1b/pf_*.jsonl)
+  static constexpr int PFL_T[16] = {0, 0, 0, 0, 0, 0, 1, 1, 2, 1, 1, 2, 2, 2, 2, 2};
+  static constexpr int PFL_DEF = PFL_T[N];
 };
 
 // sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs
@@ -211,6 +207,11 @@ __device__ __forceinline__ double ldG(const double* p) {
   if constexpr (CS) return __ldcs(p);
   else return __ldg(p);
 }
+template <bool CS>
+__device__ __forceinline__ double2 ldG2(const double2* p) {
+  if constexpr (CS) return __ldcs(p);
+  else return __ldg(p);
+}
 
 // ASM: 0 = fused scatter-add into assembled storage (fp64 RED / store); 1 = write y_L per slot
 // (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L;
@@ -250,44 +251,22 @@ __device__ __forceinline__ void eo_apply_sink(const double* __restrict__ sM, con
 }
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0,
-          bool PFL = LinesShape<N>::PFL_DEF,
-          bool GCS = true, int ASM = 0, bool PFN = false, bool PIPE = false, bool GSM = false, int STRM = -1>
+          int PFL = LinesShape<N>::PFL_DEF,
+          bool GCS = true, int ASM = 0, bool PFN = false>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
   constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB, SLAB = S::SLAB;
-  // PIPE (asynchronous gather, one element ahead): while element e is computed, the index
-  // block and then the gathered x values of this CTA's next element are copied global ->
-  // shared with cp.async (no registers held), so P1 starts from shared memory instead of two
-  // dependent HBM round trips; the index column is read back from shared memory in P5.
-  static_assert(!PIPE || (!HALO && ASM == 0), "PIPE: fused scatter-add, owned-only gather");
-  // GSM (small N, several elements per CTA): the group's G arrives in shared memory by one bulk
-  // copy issued at the top of the group iteration; P3 reads it from there (no LSU wavefronts
-  // for the 48 N_L-byte stream, which otherwise saturate L1 at N <= 4)
-  static_assert(!(PIPE && GSM), "PIPE and GSM are separate variants");
-  constexpr int NB = PIPE ? 4 : 3;  // element buffers: [u0 (u1)] r s
-  constexpr bool STREAM = STRM < 0 ? S::STREAM : (STRM > 0);  // streaming line contractions
   extern __shared__ double smem[];
   const int t = threadIdx.x;
   const int le = t / NP2;
   const int c = t - le * NP2;
   const int ca = c % NP, cb = c / NP;  // (i,j) for columns, (j,k) for rows, (i,k) for s-lines
   double* s_u = smem + (0 * EPB + le) * SLAB;
-  double* s_r = smem + ((NB - 2) * EPB + le) * SLAB;
-  double* s_s = smem + ((NB - 1) * EPB + le) * SLAB;
-  double* s_D = smem + NB * EPB * SLAB;  // folded D
-  double* s_DT = s_D + S::MAT;           // folded D^T
-  // PIPE: per-thread index columns [2][EPB][NP3] (each thread only ever reads what it copied)
-  int32_t* s_ix = reinterpret_cast<int32_t*>(s_D + S::CONST) + le * NP3 + c;
-  auto U = [&](int b) { return smem + (b * EPB + le) * SLAB; };
-  auto IX = [&](int b) { return s_ix + b * EPB * NP3; };
-  int pb = 0;
-  double* s_G = s_D + S::CONST;  // GSM: [EPB][NP][6][NP2]
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_G + EPB * 6 * NP3);
-  uint32_t gphase = 0;
-  if constexpr (GSM) {
-    if (t == 0) mbar_init(s_bar, 1);
-  }
+  double* s_r = smem + (1 * EPB + le) * SLAB;
+  double* s_s = smem + (2 * EPB + le) * SLAB;
+  double* s_D = smem + 3 * EPB * SLAB;  // folded D
+  double* s_DT = s_D + S::MAT;          // folded D^T
   for (int q = t; q < S::CONST; q += S::BLOCK) s_D[q] = __ldg(&g_EO[N][q]);  // folded D | D^T
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
   double en = 0.0;  // element energy u.(S_e u) (+ lambda u.B u) of this thread's nodes
@@ -305,18 +284,6 @@ ax_lines(const AxArgs a) {
         }
       }
   }
-  if constexpr (PIPE) {  // prologue: index column, then the gathered u column of the first element
-    const int64_t e0 = a.e_begin + (int64_t)blockIdx.x * EPB + le;
-    if (e0 < a.e_end) {
-#pragma unroll
-      for (int k = 0; k < NP; ++k) cp_async4(IX(0) + k * NP2, a.idx + e0 * NP3 + k * NP2 + c);
-      cp_async_commit();
-      cp_async_wait_all();
-#pragma unroll
-      for (int k = 0; k < NP; ++k) cp_async8(U(0) + S::at(ca, cb, k), a.x + IX(0)[k * NP2]);
-      cp_async_commit();
-    }
-  }
   __syncthreads();
 
   for (int64_t base = a.e_begin + (int64_t)blockIdx.x * EPB; base < a.e_end; base += (int64_t)gridDim.x * EPB) {
@@ -332,22 +299,6 @@ ax_lines(const AxArgs a) {
     }
     const int64_t e = base + le;
     const bool act = (e < a.e_end);
-    const int64_t e_nx = e + (int64_t)gridDim.x * EPB;  // this thread's next element (PIPE)
-    if constexpr (GSM) {
-      if (t == 0) {
-        const int64_t ne = (a.e_end - base) < EPB ? (a.e_end - base) : EPB;
-        bulk_g2s(s_G, a.G + base * 6 * NP3, (uint32_t)(ne * 48 * NP3), s_bar);
-      }
-    }
-    if constexpr (PIPE) {
-      s_u = U(pb);
-      cp_async_wait_all();  // this thread's column of u_e has landed
-      if (e_nx < a.e_end) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k) cp_async4(IX(pb ^ 1) + k * NP2, a.idx + e_nx * NP3 + k * NP2 + c);
-        cp_async_commit();
-      }
-    }
 
     // Early L2 prefetch of this element's geometric factors (consumed in P3, after the
     // gather and two barriers) and of the next element's index block (next P1).
@@ -356,18 +307,16 @@ ax_lines(const AxArgs a) {
         // PFN: fetch the NEXT element's G one whole element ahead (the first element at the
         // first iteration); otherwise this element's G at the start of its gather
         const int64_t eg = PFN ? e + (int64_t)gridDim.x * EPB : e;
-        if (PFN && base == a.e_begin + (int64_t)blockIdx.x * EPB) {
-          const char* g0 = reinterpret_cast<const char*>(a.G + e * (6 * NP3));
-          for (int q = t - le * NP2; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(g0 + q * 128);
-        }
-        if (eg < a.e_end) {
-          const char* gb = reinterpret_cast<const char*>(a.G + eg * (6 * NP3));
-#ifdef HB_PFL_BULK
-          if (c == 0) prefetch_l2_bulk(gb, 48 * NP3);
-#else
-          for (int q = t - le * NP2; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(gb + q * 128);
-#endif
-        }
+        auto pf_G = [&](int64_t ee) {
+          const char* gb = reinterpret_cast<const char*>(a.G + ee * (6 * NP3));
+          if constexpr (PFL == 2) {
+            if (c == 0) prefetch_l2_bulk(gb, 48 * NP3);
+          } else {
+            for (int q = c; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(gb + q * 128);
+          }
+        };
+        if (PFN && base == a.e_begin + (int64_t)blockIdx.x * EPB) pf_G(e);
+        if (eg < a.e_end) pf_G(eg);
         const int64_t en = e + (int64_t)gridDim.x * EPB;
         if (en < a.e_end) {
           const char* ib = reinterpret_cast<const char*>(a.idx + en * NP3);
@@ -383,7 +332,7 @@ ax_lines(const AxArgs a) {
     {
       double col[1][NP];
 #pragma unroll
-      for (int k = 0; k < NP; ++k) gi[k] = (act && ASM != 2 && !PIPE) ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
+      for (int k = 0; k < NP; ++k) gi[k] = (act && ASM != 2) ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
       if constexpr (ASM == 3) {
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
@@ -393,7 +342,6 @@ ax_lines(const AxArgs a) {
       }
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        if constexpr (PIPE) { col[0][k] = act ? s_u[S::at(ca, cb, k)] : 0.0; continue; }
         if constexpr (ASM == 2) col[0][k] = act ? __ldg(a.xh + e * NP3 + k * NP2 + c) : 0.0;  // x_L
         else if constexpr (ASM == 3) col[0][k] = act ? fma(beta, __ldg(a.xh + gi[k]), __ldg(a.x + gi[k])) : 0.0;
         else col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
@@ -409,7 +357,7 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
-    if constexpr (STREAM) {
+    if constexpr (S::STREAM) {
       double in[NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(m, ca, cb)];
@@ -432,34 +380,22 @@ ax_lines(const AxArgs a) {
       }
     }
     __syncthreads();
-    if constexpr (PIPE) {  // gather the next element's u column into the other buffer
-      if (e_nx < a.e_end) {
-        cp_async_wait_all();
-        double* un = U(pb ^ 1);
-        const int32_t* ix = IX(pb ^ 1);
-#pragma unroll
-        for (int k = 0; k < NP; ++k) cp_async8(un + S::at(ca, cb, k), a.x + ix[k * NP2]);
-        cp_async_commit();
-      }
-    }
 
     // ---- P3: metric at the (i,j) column nodes
     {
-      if constexpr (GSM) {
-        mbar_wait(s_bar, gphase);
-        gphase ^= 1u;
-      }
-      const double* Ge = GSM ? s_G + le * (6 * NP3) + c : a.G + e * (6 * NP3) + c;
+      const double* Ge = a.G + e * (6 * NP3);
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         double grr = 0, grs = 0, grt = 0, gss = 0, gst = 0, gtt = 0;
         if (act) {
-          const double* g = Ge + k * 6 * NP2;
           // G is read exactly once per apply: streaming (evict-first) loads keep it from
           // displacing the gathered x / accumulated Ap lines that neighbouring elements reuse
-          if constexpr (GSM) {
-            grr = g[0]; grs = g[NP2]; grt = g[2 * NP2]; gss = g[3 * NP2]; gst = g[4 * NP2]; gtt = g[5 * NP2];
+          if constexpr (g_pairs(N)) {
+            const double2* g2 = reinterpret_cast<const double2*>(Ge + g_off(true, NP2, k, 0, c));
+            const double2 p0 = ldG2<GCS>(g2), p1 = ldG2<GCS>(g2 + NP2), p2 = ldG2<GCS>(g2 + 2 * NP2);
+            grr = p0.x; grs = p0.y; grt = p1.x; gss = p1.y; gst = p2.x; gtt = p2.y;
           } else {
+            const double* g = Ge + g_off(false, NP2, k, 0, c);
             grr = ldG<GCS>(g); grs = ldG<GCS>(g + NP2); grt = ldG<GCS>(g + 2 * NP2);
             gss = ldG<GCS>(g + 3 * NP2); gst = ldG<GCS>(g + 4 * NP2); gtt = ldG<GCS>(g + 5 * NP2);
           }
@@ -474,7 +410,7 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
-    if constexpr (STREAM) {
+    if constexpr (S::STREAM) {
       double in[NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[m] = s_r[S::at(m, ca, cb)];
@@ -503,7 +439,6 @@ ax_lines(const AxArgs a) {
       // node k of the (i,j) column: sum the three directions, lambda terms, assembly Z^T
       auto node = [&](int k, double vtk) {
         const int o = S::at(ca, cb, k);
-        if constexpr (PIPE) gi[k] = IX(pb)[k * NP2];
         double out = vtk + s_r[o] + s_s[o];
         const double uk = s_u[o];
         en = fma(uk, out, en);
@@ -529,7 +464,7 @@ ax_lines(const AxArgs a) {
           red_y<HALO>(a, gi[k], out);
         }
       };
-      if constexpr (STREAM) {
+      if constexpr (S::STREAM) {
         eo_apply_sink<N, EPBX>(s_DT, gt[0], node);
       } else {
         double vt[1][NP];
@@ -539,9 +474,7 @@ ax_lines(const AxArgs a) {
       }
     }
     __syncthreads();
-    pb ^= 1;
   }
-  if constexpr (PIPE) cp_async_wait_all();
   if (a.cg) energy_finish<S::BLOCK>(en, a, smem);
 }
 

@@ -91,14 +91,14 @@ ax_vertex(const AxArgs a) {
             us[n] = D[j][0] * u[i + 0 + 4 * k] + D[j][1] * u[i + 2 + 4 * k];
             ut[n] = D[k][0] * u[i + 2 * j + 0] + D[k][1] * u[i + 2 * j + 4];
           }
-      // ---- metric: G slab layout [k][factor][(j,i)]
+      // ---- metric: G slab layout (g_off)
       const double* gs = smem + t * S::GPAD;
       double vr[NP3], vs[NP3], vt[NP3];
 #pragma unroll
       for (int n = 0; n < NP3; ++n) {
         const int k = n >> 2, c = n & 3;
-        const double* g = gs + k * 6 * NP2 + c;
-        const double grr = g[0], grs = g[NP2], grt = g[2 * NP2], gss = g[3 * NP2], gst = g[4 * NP2], gtt = g[5 * NP2];
+        const double grr = gs[g_off(false, NP2, k, 0, c)], grs = gs[g_off(false, NP2, k, 1, c)], grt = gs[g_off(false, NP2, k, 2, c)];
+        const double gss = gs[g_off(false, NP2, k, 3, c)], gst = gs[g_off(false, NP2, k, 4, c)], gtt = gs[g_off(false, NP2, k, 5, c)];
         vr[n] = grr * ur[n] + grs * us[n] + grt * ut[n];
         vs[n] = grs * ur[n] + gss * us[n] + gst * ut[n];
         vt[n] = grt * ur[n] + gst * us[n] + gtt * ut[n];

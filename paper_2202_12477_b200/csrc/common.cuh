@@ -29,7 +29,7 @@ struct CgScalars {
 
 struct AxArgs {
   const int32_t* __restrict__ idx;  // [E][NP3] local index into [owned | halo]
-  const double* __restrict__ G;     // [E][NP][6][NP2] slab-major
+  const double* __restrict__ G;     // [E][NP][6 NP2] slab-major, see g_off
   const double* __restrict__ B;     // [E][NP3] (mass mode 1) or null
   const double* __restrict__ x;     // owned values
   const double* __restrict__ xh;    // halo values (HALO); x_L (ASM == 2); p_{j-1} (ASM == 3)
@@ -51,6 +51,16 @@ struct AxArgs {
                     // p.Ap; 2: single-launch apply (P = 1): only write the per-CTA partials,
                     // the x/r update kernel reduces them (no fence/atomic in the operator)
 };
+
+// Device layout of the six geometric factors of one element: k-layer slabs, each holding either
+// the six factors as separate NP^2 planes, or (g_pairs(N)) three interleaved pairs (rr,rs)
+// (rt,ss) (st,tt) per node (i,j): one 16-byte load per pair, a warp's load of a pair is 512
+// contiguous bytes.  Pairs measured +2..5% at N = 2, 7, 8 and -2..10% at N = 9, 10, 12, 13
+// (profiles/r1b/gp_*.jsonl).  Offset (doubles) of factor f at node (c = i + NP j, k).
+__host__ __device__ constexpr bool g_pairs(int N) { return N == 2 || N == 7 || N == 8; }
+__host__ __device__ constexpr int g_off(bool pairs, int NP2, int k, int f, int c) {
+  return pairs ? ((k * 3 + (f >> 1)) * NP2 + c) * 2 + (f & 1) : (k * 6 + f) * NP2 + c;
+}
 
 static_assert(sizeof(AxArgs) == 128, "AxArgs must stay at 128 bytes (see the comment in the struct)");
 
@@ -91,39 +101,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // Per-thread L2 prefetch of one 128-byte line (no registers, no completion tracking).
 __device__ __forceinline__ void prefetch_l2_line(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// Asynchronous global -> shared copies (LDGSTS, sm_80+): the data lands in shared memory
-// without passing through registers; completion is per thread (commit / wait groups), other
-// threads see it after the issuing thread's wait and a CTA barrier.
-__device__ __forceinline__ void cp_async4(void* s, const void* g) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* s, const void* g) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Bulk (TMA, 1-D) global -> shared copy completing on an mbarrier (transaction bytes): no
-// LSU wavefronts, no registers; one elected thread issues, every thread waits on the phase.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of dst came first
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile("{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-               "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
 }  // namespace hbk

@@ -94,29 +94,14 @@ struct AxKernel {
 };
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0,
-          bool PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false, bool PIPE = false, bool GSM = false, int STRM = -1>
+          int PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN, PIPE, GSM, STRM>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
-  k.smem = PIPE ? hbk::LinesShape<N, EPBX>::SMEM_PIPE
-                : (GSM ? hbk::LinesShape<N, EPBX>::SMEM_GSM : hbk::LinesShape<N, EPBX>::SMEM);
+  k.smem = hbk::LinesShape<N, EPBX>::SMEM;
   return k;
-}
-
-// Asynchronous-gather operator (PIPE, ax_lines.cuh) for the fused owned-only apply: env
-// HB_AX_PIPE = comma list of degrees (or "all"), HB_AX_PIPE_PFN=1 prefetches G one element ahead
-bool deg_listed(const char* var, int N) {
-  const char* v = getenv(var);
-  if (!v) return false;
-  if (!strcmp(v, "all")) return true;
-  for (const char* q = v; *q;) {
-    if (atoi(q) == N) return true;
-    while (*q && *q != ',') ++q;
-    if (*q == ',') ++q;
-  }
-  return false;
 }
 
 template <int EPB, bool HALO, bool MASSB, int MINB, int PFB = 1>
@@ -151,7 +136,7 @@ template <int N>
 AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
   constexpr int M = hbk::LinesShape<N>::MINB;
   if (halo) return massb ? make_lines<N, true, true, kLinesPF>() : make_lines<N, true, false, kLinesPF>();
-  constexpr bool PL = hbk::LinesShape<N>::PFL_DEF;
+  constexpr int PL = hbk::LinesShape<N>::PFL_DEF;
   if (asm_mode == 1)
     return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 1>()
                  : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 1>();
@@ -159,34 +144,6 @@ AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
   if (asm_mode == 3)
     return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 3>()
                  : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 3>();
-  if constexpr (N >= 2 && N <= 5) {
-    if (deg_listed("HB_AX_GSM", N)) {
-      constexpr int MG = hbk::LinesShape<N>::MINB_GSM;
-      return massb ? make_lines<N, false, true, kLinesPF, MG, 0, false, true, 0, false, false, true>()
-                   : make_lines<N, false, false, kLinesPF, MG, 0, false, true, 0, false, false, true>();
-    }
-  }
-  if (!massb && N >= 8 && deg_listed("HB_AX_STREAM", N)) {
-    // experiment: streaming line contractions (as N = 12) at other degrees; HB_AX_STREAM_MINB=1
-    // uncaps the registers (one CTA per SM), HB_AX_PIPE adds the asynchronous gather
-    constexpr int M = hbk::LinesShape<N>::MINB;
-    const char* mb = getenv("HB_AX_STREAM_MINB");
-    const bool one = mb && mb[0] == '1';
-    if (deg_listed("HB_AX_PIPE", N))
-      return one ? make_lines<N, false, false, kLinesPF, 1, 0, PL, true, 0, false, true, false, 1>()
-                 : make_lines<N, false, false, kLinesPF, hbk::LinesShape<N>::MINB_PIPE, 0, PL, true, 0, false, true, false, 1>();
-    return one ? make_lines<N, false, false, kLinesPF, 1, 0, PL, true, 0, false, false, false, 1>()
-               : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 0, false, false, false, 1>();
-  }
-  if (deg_listed("HB_AX_PIPE", N)) {
-    constexpr int MP = hbk::LinesShape<N>::MINB_PIPE;
-    const char* pfn = getenv("HB_AX_PIPE_PFN");
-    if (pfn && pfn[0] == '1')
-      return massb ? make_lines<N, false, true, kLinesPF, MP, 0, true, true, 0, true, true>()
-                   : make_lines<N, false, false, kLinesPF, MP, 0, true, true, 0, true, true>();
-    return massb ? make_lines<N, false, true, kLinesPF, MP, 0, PL, true, 0, false, true>()
-                 : make_lines<N, false, false, kLinesPF, MP, 0, PL, true, 0, false, true>();
-  }
   return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
 }
 
@@ -276,7 +233,7 @@ AxKernel pick_ax(int N, bool halo, bool massb, int asm_mode = 0) {
   }
 }
 
-// packed host G [E][NP3][6] -> device layout [E][NP][6][NP2]
+// packed host G [E][NP3][6] -> device layout [E][NP][6 NP2] (hbk::g_off)
 __global__ void relayout_G(const double* __restrict__ src, double* __restrict__ dst, int64_t E, int NP) {
   const int NP2 = NP * NP, NP3 = NP2 * NP;
   const int64_t total = E * NP3;
@@ -284,7 +241,7 @@ __global__ void relayout_G(const double* __restrict__ src, double* __restrict__ 
     int64_t e = s / NP3;
     int n = (int)(s - e * NP3);
     int k = n / NP2, c = n - k * NP2;
-    for (int f = 0; f < 6; ++f) dst[((e * NP + k) * 6 + f) * NP2 + c] = src[s * 6 + f];
+    for (int f = 0; f < 6; ++f) dst[e * 6 * NP3 + hbk::g_off(hbk::g_pairs(NP - 1), NP2, k, f, c)] = src[s * 6 + f];
   }
 }
 
@@ -298,9 +255,10 @@ __global__ void box_G(double* __restrict__ dst, int64_t E, int N, double grr, do
     int k = n / NP2, c = n - k * NP2;
     int i = c % NP, j = c / NP;
     double wq = hbk::c_D[0][i] * hbk::c_D[0][j] * hbk::c_D[0][k];  // weights staged in c_D[0]
-    double* d = dst + ((e * NP + k) * 6) * NP2 + c;
-    d[0] = wq * grr; d[NP2] = 0.0; d[2 * NP2] = 0.0;
-    d[3 * NP2] = wq * gss; d[4 * NP2] = 0.0; d[5 * NP2] = wq * gtt;
+    double* d = dst + e * 6 * NP3;
+    const bool gp = hbk::g_pairs(N);
+    d[hbk::g_off(gp, NP2, k, 0, c)] = wq * grr; d[hbk::g_off(gp, NP2, k, 1, c)] = 0.0; d[hbk::g_off(gp, NP2, k, 2, c)] = 0.0;
+    d[hbk::g_off(gp, NP2, k, 3, c)] = wq * gss; d[hbk::g_off(gp, NP2, k, 4, c)] = 0.0; d[hbk::g_off(gp, NP2, k, 5, c)] = wq * gtt;
   }
 }
 

@@ -689,7 +689,7 @@ __global__ void jacobi_diag_kernel(const double* __restrict__ G, const int32_t* 
     const int n = (int)(s - e * NP3);
     const int k = n / NP2, c = n - k * NP2, i = c % NP, j = c / NP;
     const double* Ge = G + e * 6 * NP3;
-    auto g = [&](int f, int ii, int jj, int kk) { return Ge[(kk * 6 + f) * NP2 + jj * NP + ii]; };
+    auto g = [&](int f, int ii, int jj, int kk) { return Ge[g_off(g_pairs(N), NP2, kk, f, jj * NP + ii)]; };
     double d = 0.0;
     for (int m = 0; m < NP; ++m) {
       d += D[m * NP + i] * D[m * NP + i] * g(0, m, j, k);
