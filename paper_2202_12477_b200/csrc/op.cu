@@ -173,6 +173,9 @@ AxKernel tune_variant(int v) {
     case 6: return make_lines<N, false, false, 0, tune_minb<N, E128, 128>(), E128>();
     case 7: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, true, true, 0, true>();  // G one element ahead
     case 8: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, false>();                // no G prefetch
+    case 9: return make_lines<N, false, false, 0, tune_minb<N, 0, 112>()>();   // 112 regs
+    case 10: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>()>();   // 96 regs
+    case 11: return make_lines<N, false, false, 0, tune_minb<N, 0, 80>()>();   // 80 regs
     default: return make_lines<N, false, false, kLinesPF>();
   }
 }

@@ -83,7 +83,7 @@ def test_apply_all_degrees_random_geometry(hb, N):
     check_apply(hb, box, N, 1.0, 0, True, seed=N)
 
 
-@pytest.mark.parametrize("N", [1, 3, 7, 9, 15])
+@pytest.mark.parametrize("N", [1, 2, 3, 7, 9, 15])
 @pytest.mark.parametrize("mass_mode,lam", [(0, 0.0), (0, 2.5), (1, 1.0)])
 def test_apply_modes(hb, N, mass_mode, lam):
     box = (2, 3, 1)
@@ -262,7 +262,7 @@ def test_loopback_group_apply_and_cg(hb, P):
     assert np.abs(x - xo).max() <= 1e-10 * np.abs(xo).max()
 
 
-@pytest.mark.parametrize("box,N", [((52, 52, 52), 7), ((24, 24, 24), 15), ((122, 122, 122), 3), ((120, 100, 91), 1)])
+@pytest.mark.parametrize("box,N", [((52, 52, 52), 7), ((24, 24, 24), 15), ((122, 122, 122), 3), ((120, 100, 91), 1), ((184, 184, 184), 2)])
 def test_full_size_C3_sampled_and_properties(hb, box, N):
     """C3 at full size (~50 M DOFs), the launch configuration bench.py / opbench time:
     sampled entries against the oracle computed one by one (c17 scale from |D|, |G|), plus
@@ -409,7 +409,7 @@ def test_tolerance_mode_device_graph_matches_host_loop(hb, monkeypatch):
     assert j == 7 and len(h) == 8
 
 
-@pytest.mark.parametrize("N,mass_mode", [(3, 0), (5, 1), (7, 0)])
+@pytest.mark.parametrize("N,mass_mode", [(2, 1), (3, 0), (5, 1), (7, 0), (8, 1)])  # 2, 7, 8: factor-pair G layout
 def test_jacobi_pcg(hb, N, mass_mode, monkeypatch):
     """Jacobi-preconditioned CG (NEXT #3): diag(A) against the oracle's assembled element
     diagonals; PCG iterates (fixed and tolerance modes, device-graph and host loops) against
