@@ -144,7 +144,12 @@ def run_reference(args):
     N = args.N
     import numpy as np
     from oracle import basis, cg as ocg, forcing as of, mesh as om, operator as oo
+    from oracle import partition as opart
     from paper_2202_12477_b200 import ledger
+    blk = box
+    if args.gpus > 1 and not args.strong:  # the GPU arm's weak-scaling box: per-GPU block x rank grid
+        g = opart.rank_grid(args.gpus, 64, 64, 64)
+        box = (box[0] * g[0], box[1] * g[1], box[2] * g[2])
     x, w, D = basis.basis(N)
     E, NG, NL = om.global_sizes(*box, N)
     gid = om.l2g(*box, N)
@@ -169,8 +174,10 @@ def run_reference(args):
     sample = f"{k} CG iterations per step (of {args.iters}) of box {box[0]}x{box[1]}x{box[2]} N={N}"
     out = {"impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"C2: N={N}, E={box[0]}x{box[1]}x{box[2]}, {args.iters} CG iterations (sampled)",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": "strong" if args.strong else "weak",
+           "config": {"workload": f"{'C2' if blk == (16, 16, 16) and N == 7 else 'custom'}: N={N}, "
+                                  f"E={box[0]}x{box[1]}x{box[2]}, {args.iters} CG iterations (sampled)",
                       "box": list(box), "N": N, "N_G": NG, "lambda": 1.0},
            "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
