@@ -312,14 +312,14 @@ ax_lines(const AxArgs a) {
         const int64_t eg = PFN ? e + (int64_t)gridDim.x * EPB : e;
         auto pf_G = [&](int64_t ee) {
           const char* gb = reinterpret_cast<const char*>(a.G + ee * (6 * NP3));
-          if constexpr (PFL >= 2) {
+          if constexpr (PFL == 2) {
             if (c == 0) prefetch_l2_bulk(gb, 48 * NP3);
           } else {
             for (int q = c; q < (6 * NP3 * 8) / 128; q += NP2) prefetch_l2_line(gb + q * 128);
           }
         };
-        if ((PFN || PFL == 3) && base == a.e_begin + (int64_t)blockIdx.x * EPB) pf_G(e);
-        if (PFL != 3 && eg < a.e_end) pf_G(eg);
+        if (PFN && base == a.e_begin + (int64_t)blockIdx.x * EPB) pf_G(e);
+        if (eg < a.e_end) pf_G(eg);
         const int64_t en = e + (int64_t)gridDim.x * EPB;
         if (en < a.e_end) {
           const char* ib = reinterpret_cast<const char*>(a.idx + en * NP3);
@@ -408,10 +408,6 @@ ax_lines(const AxArgs a) {
         s_r[o] = grr * ur + grs * us + grt * ut;
         s_s[o] = grs * ur + gss * us + gst * ut;
         gt[0][k] = grt * ur + gst * us + gtt * ut;
-      }
-      if constexpr (PFL == 3) {  // this element's G is loaded: bulk-prefetch the next element's
-        const int64_t en = e + (int64_t)gridDim.x * EPB;
-        if (act && c == 0 && en < a.e_end) prefetch_l2_bulk(a.G + en * (6 * NP3), 48 * NP3);
       }
     }
     __syncthreads();

@@ -176,7 +176,6 @@ AxKernel tune_variant(int v) {
     case 9: return make_lines<N, false, false, 0, tune_minb<N, 0, 112>()>();   // 112 regs
     case 10: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>()>();   // 96 regs
     case 11: return make_lines<N, false, false, 0, tune_minb<N, 0, 80>()>();   // 80 regs
-    case 12: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, 3>();  // bulk G of the next element after P3
     case 13: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, 2>();  // bulk G of this element
     default: return make_lines<N, false, false, kLinesPF>();
   }
