@@ -304,6 +304,7 @@ struct hb_op {
   bool scat_mode = false;  // operator launches read x_L (sL_p) and write y_L
   DevBuf sL_x, sL_r, sL_p, sL_w, sW;
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
+  hbk::CondTest cond_test = {0, 0.0, 0, 0};  // set while the tolerance graph's WHILE body is captured
   const void* fused_fn = nullptr;  // cg_update_fused<U> instance (U double2 per thread per batch)
   bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
@@ -1190,7 +1191,8 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
     double* hp = op->hist.as<double>();
     const double* ivd = op->jacobi ? op->invd.as<double>() : nullptr;
     double* rzp = op->rz_part.as<double>();
-    void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &ppp, &lpp, &li, &rrp, &s, &hp, &ivd, &rzp};
+    hbk::CondTest ct = op->cond_test;
+    void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &ppp, &lpp, &li, &rrp, &s, &hp, &ivd, &rzp, &ct};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(op->fused_grid); cfg.blockDim = dim3(hbk::VEC_BLOCK); cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -1441,8 +1443,12 @@ int cg_tol_graph(hb_op* op, const double* b, double* x, int32_t max_iters, doubl
       fail(cudaStreamBeginCaptureToGraph(cs2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
            "begin body capture");
       if (status == HB_OK) {
+        // with the fused vector update the loop test runs inside it (no separate kernel)
+        const bool folded = op->fused_grid > 0;
+        if (folded) op->cond_test = hbk::CondTest{h, eps, max_iters, 1};
         status = cg_iteration(op, x, cs2);
-        if (status == HB_OK) {
+        op->cond_test.on = 0;
+        if (status == HB_OK && !folded) {
           hbk::cg_continue<<<1, 1, 0, cs2>>>(h, s, eps, max_iters, 0);
           fail(cudaGetLastError(), "cg_continue");
         }
@@ -1466,7 +1472,7 @@ int cg_tol_graph(hb_op* op, const double* b, double* x, int32_t max_iters, doubl
   CU_TRY(cudaStreamSynchronize(st));
   const hbk::CgScalars* hs = reinterpret_cast<const hbk::CgScalars*>(op->host_scal);
   const int32_t iters = hs->it;
-  op->launches += 1 + (int64_t)iters * 3;  // init + (operator, update, loop test) per trip
+  op->launches += 1 + (int64_t)iters * (op->fused_grid > 0 ? 2 : 3);  // init + (operator, update[, loop test]) per trip
   if (hs->flags & 1) {
     set_error("hb_cg_solve: breakdown (p.Ap <= 0 or non-finite) at iteration " + std::to_string(iters - 1));
     return HB_ERR_BREAKDOWN;

@@ -176,6 +176,25 @@ cg_update_xr_e(double* __restrict__ x, const double* __restrict__ p, double* __r
   }
 }
 
+// Tolerance-mode loop test folded into the fused vector update (the WHILE body's last kernel
+// publishes the scalars anyway): Alg. 1 line 6 (while r.r > eps), the iteration cap and
+// the breakdown check (p.Ap <= 0 or non-finite) set the WHILE node's condition -- one launch
+// per trip fewer than a separate cg_continue kernel.
+struct CondTest {
+  cudaGraphConditionalHandle h;
+  double eps;
+  int32_t max_iters;
+  int32_t on;
+};
+__device__ __forceinline__ void cond_test(const CondTest& ct, CgScalars* s, double pAp, double rr_new, int32_t it) {
+  bool go = rr_new > ct.eps && it < ct.max_iters;
+  if (!(pAp > 0.0) || !isfinite(pAp) || !isfinite(rr_new)) {
+    s->flags |= 1;
+    go = false;
+  }
+  cudaGraphSetConditional(ct.h, go ? 1u : 0u);
+}
+
 // One GPU, whole vector update of an iteration in one cooperative kernel (grid barrier
 // instead of a kernel boundary): p.Ap = sum(e_part) + lambda sum(pp_part) (deterministic,
 // every CTA alike); x += alpha p, r -= alpha Ap, CTA partial of r.r; grid barrier; every CTA
@@ -187,7 +206,7 @@ __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_fused0(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
                 double lam_init, double* rr_part, CgScalars* s, double* hist, const double* __restrict__ invd,
-                double* rz_part) {
+                double* rz_part, CondTest ct) {
   __shared__ double s_b[3];
   pdl_wait();
   // ---- p.Ap and alpha (identical in every CTA)
@@ -289,6 +308,7 @@ cg_update_fused0(double* __restrict__ x, double* __restrict__ p, double* __restr
       s->rr_new = rr_new;
       s->rz = rho_new;
       s->it += 1;
+      if (ct.on) cond_test(ct, s, pAp, rr_new, s->it);
     }
   }
 }
@@ -298,7 +318,7 @@ __global__ void __launch_bounds__(VEC_BLOCK, MINB)
 cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
                 double lam_init, double* rr_part, CgScalars* s, double* hist, const double* __restrict__ invd,
-                double* rz_part) {
+                double* rz_part, CondTest ct) {
   // U double2 per thread per batch: every load of a batch is issued before any use, and the
   // first batch is in flight while the CTA reduces the p.Ap partials.  When a thread's whole
   // share fits one batch, the p update reuses the registers (r_{j+1}, p_j, M^-1) -- no re-read.
@@ -435,6 +455,7 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       s->rr_new = rr_new;
       s->rz = rho_new;
       s->it += 1;
+      if (ct.on) cond_test(ct, s, pAp, rr_new, s->it);
     }
   }
 }
