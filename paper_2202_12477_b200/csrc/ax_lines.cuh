@@ -74,8 +74,9 @@ struct LinesShape {
   static constexpr bool STREAM = N == 12;
   // N = 13: one uncapped CTA per SM since the bulk G prefetch (0.61 vs 0.57 at 2 x 128 registers,
   // profiles/r1b/tune3.jsonl); N = 7: 96 registers (10 CTAs per SM) since the factor-pair G
-  // layout (0.962 vs 0.943 at C3, equal at C2; profiles/r1b/tune_n7_regs.jsonl)
-  static constexpr int REGS_T[16] = {0, 64, 64, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 0, 0, 0};
+  // layout (0.962 vs 0.943 at C3, equal at C2; profiles/r1b/tune_n7_regs.jsonl); N = 2: 80 registers
+  // (0.614 vs 0.607, three repeats each; profiles/r1b/last_ab_n2regs_n13pad.jsonl)
+  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 0, 0, 0};
   static constexpr int REGS = REGS_T[N];
   static constexpr int MINB_REG0 = REGS ? 65536 / (BLOCK * REGS) : 1;
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
