@@ -178,7 +178,7 @@ int hb_dot(hb_op* op, const double* a_dev, const double* b_dev, double* out_host
  * r.r <= eps (absolute, c14) or j == max_iters; HB_ERR_BREAKDOWN if p.Ap <= 0 or
  * non-finite.  With P = 1 tolerance mode is also one CUDA graph: a WHILE conditional node
  * whose loop test (r.r > eps, j < max_iters, no breakdown) runs on the device, so the host
- * synchronises only at the end (env HB_TOL_GRAPH=0 selects a host-driven loop).  rr_hist_host (nullable) receives r_j.r_j for j = 0..iterations
+ * synchronises only at the end (hb_op_set_tolerance_loop(op, 0) selects a host-driven loop).  rr_hist_host (nullable) receives r_j.r_j for j = 0..iterations
  * ([max_iters+1]).  x_dev receives the solution [n_owned].  Synchronises the stream at the end. */
 int hb_cg_solve(hb_op* op, const double* b_dev, double* x_dev, int32_t max_iters, double eps,
                 double* rr_hist_host, hb_cg_result* res, void* stream);
@@ -197,14 +197,9 @@ int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host, int32_t ma
 /* Assembly variant: 0 (default) = Z^T fused into the operator as fp64 scatter-add (atomic
  * accumulation order, results reproducible to rounding); 1 = the paper's split form (P:154,
  * P:219): the operator writes y_L per slot and a CSR gather kernel sums every DOF's slots in
- * ascending (e, n) order -- bitwise reproducible, +20 N_L bytes per apply; 2 = as 0, and
- * fixed-mode CG moves Alg. 1's p update into the next operator: its gather forms
- * p_j = r_j + beta_j p_{j-1} from r and the previous p (two alternating buffers), the first
- * slot (e, n) of every DOF stores p_j and adds lambda W u once (Z^T lambda W Z = lambda I, c1),
- * and one barrier-free vector kernel does alpha, x, r, r.r, beta and re-zeroes Ap
- * (96 N_G + 52 N_L bytes per iteration instead of 104 N_G + 52 N_L; same iterates up to
- * rounding).  Applies and tolerance mode are unchanged.  Variants 1 and 2: P = 1 only
- * (HB_ERR_STATE otherwise).  Synchronous (builds the CSR / designated slots on first use). */
+ * ascending (e, n) order -- bitwise reproducible, +20 N_L bytes per apply.  Variant 1: P = 1
+ * only (HB_ERR_STATE otherwise); HB_ERR_ARG for any other value.  Synchronous (builds the CSR
+ * on first use). */
 int hb_op_set_variant(hb_op* op, int variant, void* stream);
 /* Jacobi-preconditioned CG (NekBone's diagonal preconditioner, P:140 --
  * hipBone itself uses none).  enable = 1 computes M = diag(A) on the device once
@@ -214,6 +209,16 @@ int hb_op_set_variant(hb_op* op, int variant, void* stream);
  * hb_op_jacobi_diagonal writes diag(A) [n_owned] to a device buffer (test hook). */
 int hb_op_set_jacobi(hb_op* op, int enable, void* stream);
 int hb_op_jacobi_diagonal(hb_op* op, double* diag_dev, void* stream);
+/* Tolerance-mode loop of hb_cg_solve (P = 1): device = 1 (default) runs the loop test on the
+ * device inside one CUDA graph (WHILE conditional node); device = 0 runs a host-driven loop that
+ * reads r.r back every iteration (the reference behaviour for tests).  HB_ERR_ARG otherwise. */
+int hb_op_set_tolerance_loop(hb_op* op, int device);
+/* Launch shape of the operator kernel used by hb_op_apply / hb_cg_solve on the rank's
+ * interior elements: out[0] = resident grid (CTAs the kernel launches at most; it loops over
+ * elements beyond that), out[1] = threads per CTA, out[2] = elements per CTA per loop trip,
+ * out[3] = dynamic shared memory bytes per CTA.  Host-only query (test hook: parity cases
+ * size their meshes to several grid waves). */
+int hb_op_launch_shape(const hb_op* op, int32_t out[4]);
 /* Profiling of the operator kernel inside hb_cg_solve / hb_op_apply: enable = k > 0 brackets
  * every k-th operator launch with CUDA events on its stream (inside captured graphs as event
  * nodes); enable = 0 turns it off.  hb_op_kernel_time returns the number of timed launches

@@ -23,6 +23,7 @@ Modules
   ledger     FLOP / byte / roofline formulas
 
 Parity status: every function is pinned by ``tests/test_oracle_*.py`` (closed forms,
-invariants, brute force, golden values); see DESIGN.md "Oracle pins". There is no
-"parity unpinned" function in this package.
+invariants, brute force, golden values), including the parity checkers apply_abs,
+apply_abs_explicit and apply_entries and the owner rule; see DESIGN.md section 7 and
+reading R5. There is no "parity unpinned" function in this package.
 """

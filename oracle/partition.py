@@ -63,6 +63,14 @@ def element_rank(nx, ny, nz, grid) -> np.ndarray:
     return er
 
 
+def owner_of(g: int, sharers_sorted, seed: int) -> int:
+    """Owner of global id g among its sharing ranks ("randomly, but fairly"; reading c9):
+    sorted_sharers[splitmix64(splitmix64(seed) XOR g) mod k]; a node with one sharer is its own."""
+    if len(sharers_sorted) == 1:
+        return sharers_sorted[0]
+    return sharers_sorted[splitmix64(splitmix64(seed) ^ g) % len(sharers_sorted)]
+
+
 def build(nx, ny, nz, N, P, seed=0, grid=None):
     """Per-rank partition data for every rank (dict list)."""
     if grid is None:
@@ -73,11 +81,7 @@ def build(nx, ny, nz, N, P, seed=0, grid=None):
     for e in range(gid_all.shape[0]):
         for g in gid_all[e]:
             sharers.setdefault(int(g), set()).add(int(er[e]))
-    seed_h = splitmix64(seed)
-    owner = {}
-    for g, s in sharers.items():
-        srt = sorted(s)
-        owner[g] = srt[0] if len(srt) == 1 else srt[splitmix64(seed_h ^ g) % len(srt)]
+    owner = {g: owner_of(g, sorted(s), seed) for g, s in sharers.items()}
     ranks = []
     for r in range(P):
         mine = [e for e in range(gid_all.shape[0]) if er[e] == r]
@@ -104,7 +108,7 @@ def build(nx, ny, nz, N, P, seed=0, grid=None):
         for q in neighbors:
             q_refs = {int(g) for e in range(gid_all.shape[0]) if er[e] == q for g in gid_all[e]}
             send[q] = sorted(g for g in owned if g in q_refs)
-        ranks.append(dict(grid=grid, elements=order, nA=len(A), nH=len(halo_e), nB=len(B),
+        ranks.append(dict(grid=grid, elements=order, owner=owner, nA=len(A), nH=len(halo_e), nB=len(B),
                           owned=owned, halo=halo, gid=gid_local, idx=idx,
                           neighbors=neighbors, recv=recv, send=send))
     return ranks

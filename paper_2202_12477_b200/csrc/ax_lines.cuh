@@ -218,10 +218,7 @@ __device__ __forceinline__ double2 ldG2(const double2* p) {
 }
 
 // ASM: 0 = fused scatter-add into assembled storage (fp64 RED / store); 1 = write y_L per slot
-// (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L;
-// 3 = fused p update (P = 1 CG): u = r + beta p_{j-1} gathered from r (x) and p_{j-1} (xh),
-// p_j stored by each DOF's designated slot (sign bit of idx), Ap zero-initialised and the
-// lambda W term added once per DOF at the designated slot (Z^T lambda W Z = lambda I, c1).
+// (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L.
 // Streaming form of eo_apply for one line: each output y_i is handed to sink(i, y_i) as soon
 // as it is formed (the input line is folded into e/o first, so it may be overwritten in place);
 // no output array is kept -- large N stays within the register budget of 2 CTAs per SM.
@@ -274,8 +271,6 @@ ax_lines(const AxArgs a) {
   for (int q = t; q < S::CONST; q += S::BLOCK) s_D[q] = __ldg(&g_EO[N][q]);  // folded D | D^T
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
   double en = 0.0;  // element energy u.(S_e u) (+ lambda u.B u) of this thread's nodes
-  double beta = 0.0;
-  if constexpr (ASM == 3) beta = a.cg->beta;
 
   if constexpr (PF > 0) {
     if (t == 0)
@@ -331,30 +326,16 @@ ax_lines(const AxArgs a) {
 
     // ---- P1: gather the (i,j) column (Z x) and the t-derivative in registers
     int32_t gi[NP];
-    uint32_t des = 0;  // ASM == 3: bit k set if slot (i,j,k) is its DOF's designated slot
     double gt[1][NP];  // ut, later the G-mixed gt
     {
       double col[1][NP];
 #pragma unroll
       for (int k = 0; k < NP; ++k) gi[k] = (act && ASM != 2) ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
-      if constexpr (ASM == 3) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          des |= (uint32_t)(gi[k] < 0) << k;
-          gi[k] &= 0x7fffffff;
-        }
-      }
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         if constexpr (ASM == 2) col[0][k] = act ? __ldg(a.xh + e * NP3 + k * NP2 + c) : 0.0;  // x_L
-        else if constexpr (ASM == 3) col[0][k] = act ? fma(beta, __ldg(a.xh + gi[k]), __ldg(a.x + gi[k])) : 0.0;
         else col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
         s_u[S::at(ca, cb, k)] = col[0][k];
-      }
-      if constexpr (ASM == 3) {
-#pragma unroll
-        for (int k = 0; k < NP; ++k)
-          if ((des >> k) & 1u) a.yh[gi[k]] = col[0][k];  // p_j = r_j + beta_j p_{j-1}, once per DOF
       }
       eo_apply<N, EPBX, 1>(s_D, col, gt);
     }
@@ -451,15 +432,7 @@ ax_lines(const AxArgs a) {
           out += lb;
           en = fma(uk, lb, en);
         }
-        if constexpr (ASM == 3) {
-          if (!MASSB && ((des >> k) & 1u)) {  // lambda W: once per DOF
-            const double lu = a.lam * uk;
-            en = fma(uk, lu, en);
-            out += lu;
-          }
-          if (interior_ij && k > 0 && k < N) a.y[gi[k]] = out;  // sole contribution: plain store
-          else atomicAdd(a.y + gi[k], out);
-        } else if constexpr (ASM >= 1) {  // y_L per slot, assembled by a CSR (gather-scatter) kernel
+        if constexpr (ASM >= 1) {  // y_L per slot, assembled by a CSR (gather-scatter) kernel
           a.yh[e * NP3 + k * NP2 + c] = out;  // y_L
         } else if (interior_ij && k > 0 && k < N) {
           if (!MASSB) out = fma(a.lam, uk, out);  // W = 1 on element-interior nodes

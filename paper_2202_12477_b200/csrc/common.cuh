@@ -19,7 +19,7 @@ struct CgScalars {
   double pp;       // local p.p (for the lambda term of the fused p.Ap)
   double e_acc;    // element-energy accumulator across the operator launches of one apply
   double rz;       // Jacobi PCG: r_j.z_j (z = M^-1 r), the rho of alpha / beta
-  double beta;     // fused-p CG (ASM == 3): beta_j, read by the operator that forms p_j
+  double spare;
   double pad;
   int32_t it;        // iteration counter j
   uint32_t ticket;   // last-CTA detection, vector kernels
@@ -32,9 +32,9 @@ struct AxArgs {
   const double* __restrict__ G;     // [E][NP][6 NP2] slab-major, see g_off
   const double* __restrict__ B;     // [E][NP3] (mass mode 1) or null
   const double* __restrict__ x;     // owned values
-  const double* __restrict__ xh;    // halo values (HALO); x_L (ASM == 2); p_{j-1} (ASM == 3)
+  const double* __restrict__ xh;    // halo values (HALO); x_L (ASM == 2)
   double* y;                        // owned output (pre-initialised)
-  double* yh;                       // halo output accumulator (HALO); y_L per slot (ASM 1, 2); p_j (ASM == 3)
+  double* yh;                       // halo output accumulator (HALO); y_L per slot (ASM 1, 2)
   // (the struct stays at 128 bytes: a larger kernel parameter block measurably changed the
   //  operator's code generation -- 10% slower at N = 7)
   int64_t e_begin, e_end;           // element range of this launch

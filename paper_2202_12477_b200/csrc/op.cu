@@ -87,6 +87,14 @@ struct DevBuf {
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// Launch-shape knobs for A/B measurements exist only in tuning builds (-DHB_TUNE, build.py
+// with HB_TUNE=1); the product library ignores the environment.
+#ifdef HB_TUNE
+const char* tune_env(const char* name) { return getenv(name); }
+#else
+const char* tune_env(const char*) { return nullptr; }
+#endif
+
 struct AxKernel {
   const void* fn = nullptr;
   int block = 0, epb = 0, grid_max = 0;
@@ -116,10 +124,10 @@ AxKernel make_vertex() {
 
 // N = 1, fused scatter-add: one element per thread (ax_vertex.cuh), 64 elements per CTA
 // with an L2 prefetch of G one grid batch ahead (C3: 3.86 ms = 0.86 of peak; no prefetch
-// 4.59 ms, line kernel 5.56 ms); env HB_N1_LINES=1, HB_N1_EPB=32|64|128, HB_N1_PF=0|1|2 for A/B
+// 4.59 ms, line kernel 5.56 ms); tuning builds: HB_N1_LINES=1, HB_N1_EPB=32|64|128, HB_N1_PF=0|1|2
 AxKernel pick_vertex(bool halo, bool massb) {
-  const char* ev = getenv("HB_N1_EPB");
-  const char* pv = getenv("HB_N1_PF");
+  const char* ev = tune_env("HB_N1_EPB");
+  const char* pv = tune_env("HB_N1_PF");
   const int epb = ev ? atoi(ev) : 64, pf = pv ? atoi(pv) : 1;
 #define HB_VX(E, M, P) \
   (halo ? (massb ? make_vertex<E, true, true, M, P>() : make_vertex<E, true, false, M, P>()) \
@@ -141,9 +149,6 @@ AxKernel pick_ax_n(bool halo, bool massb, int asm_mode) {
     return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 1>()
                  : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 1>();
   if (asm_mode == 2) return make_lines<N, false, false, kLinesPF, M, 0, PL, true, 2>();  // mass mode 0 only
-  if (asm_mode == 3)
-    return massb ? make_lines<N, false, true, kLinesPF, M, 0, PL, true, 3>()
-                 : make_lines<N, false, false, kLinesPF, M, 0, PL, true, 3>();
   return massb ? make_lines<N, false, true, kLinesPF>() : make_lines<N, false, false, kLinesPF>();
 }
 
@@ -215,7 +220,7 @@ AxKernel pick_ax(int N, bool halo, bool massb, int asm_mode = 0) {
   }
 #endif
   if (N == 1 && asm_mode == 0) {
-    const char* l = getenv("HB_N1_LINES");
+    const char* l = tune_env("HB_N1_LINES");
     if (!(l && l[0] == '1')) return pick_vertex(halo, massb);
   }
   switch (N) {
@@ -298,6 +303,7 @@ struct hb_op {
   DevBuf idx, G, B, owned_gid;
   DevBuf r, p, Ap, xs, partials, e_part, pp_part, rz_part, invd, scal, hist, dot_out, dot_ticket;
   bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
+  bool tol_device_loop = true;  // tolerance mode as one graph with a WHILE node (P = 1)
   int variant = 0;      // 0: fused scatter-add (fp64 RED); 1: y_L + CSR gather (deterministic), P = 1
   DevBuf yL, csr_ptr, csr_slots;
   // NekBone scattered storage (NEXT #4): local vectors of length N_L and the weights W
@@ -312,12 +318,7 @@ struct hb_op {
   std::vector<int64_t> soff, scnt, roff, rcnt;
   int64_t n_send = 0;
   int last_grid = 0;  // grid of the last operator launch (number of energy partials, P = 1)
-  AxKernel ax_plain, ax_halo, ax_yl, ax_scat, ax_fp;  // ax_yl / ax_scat / ax_fp picked on first use
-  // fused-p CG (P = 1 fixed mode): the p update runs inside the next operator (ASM == 3)
-  bool fusedp = false;
-  DevBuf idx_des, p_alt;   // idx with the designated-slot sign bit; the second p buffer
-  const double* fp_pold = nullptr;
-  double* fp_pnew = nullptr;
+  AxKernel ax_plain, ax_halo, ax_yl, ax_scat;  // ax_yl / ax_scat picked on first use
   cudaStream_t comm_stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture (the legacy stream cannot be captured)
   cudaStream_t cap_stream2 = nullptr; // captures the body of the tolerance-mode WHILE node
@@ -424,11 +425,6 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.e_begin = e0; a.e_end = e1;
   a.n_owned = (int32_t)op->sz.n_owned;
   a.halo_mode = 0;
-  if (op->fp_pnew) {  // ASM == 3: x = r_j, xh = p_{j-1}, yh = p_j, idx with designated bits
-    a.idx = op->idx_des.as<int32_t>();
-    a.xh = op->fp_pold;
-    a.yh = op->fp_pnew;
-  }
   if (op->halo_mode_now) {
     a.halo_mode = 1;
     a.xh = op->hx_tab.as<double>();
@@ -909,8 +905,8 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     int dev = 0, coop = 0, nb = 0;
     CU_TRY(cudaGetDevice(&dev));
     CU_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    const char* ue = getenv("HB_UPD_U");
-    const char* me = getenv("HB_UPD_MINB");
+    const char* ue = tune_env("HB_UPD_U");
+    const char* me = tune_env("HB_UPD_MINB");
     // default: the batched form (first batch in flight during the p.Ap reduction) for vectors that
     // fit L2 (C2: +1.3%), the single-item form above that (C3 N=7: the batched one is 2.7% slower;
     // profiles/r1_update_ab.jsonl)
@@ -924,14 +920,14 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
       op->fused_fn = U >= 4 ? (const void*)&hbk::cg_update_fused<4, 1>
                    : U == 2 ? (const void*)&hbk::cg_update_fused<2, 1> : (const void*)&hbk::cg_update_fused<1, 1>;
     CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, op->fused_fn, hbk::VEC_BLOCK, 0));
-    const char* env = getenv("HB_FUSED_UPDATE");
+    const char* env = tune_env("HB_FUSED_UPDATE");
     if (coop && nb > 0 && !(env && env[0] == '0'))
       op->fused_grid = std::min(vec_grid(std::max<int64_t>(n, 1)), nb * num_sms());
   }
   HB_TRY(op->pp_part.alloc((size_t)std::max(op->fused_grid, 1) * 8 + 64));
   HB_TRY(op->rz_part.alloc((size_t)std::max(op->fused_grid, 1) * 8 + 64));
   {
-    const char* env = getenv("HB_PDL");
+    const char* env = tune_env("HB_PDL");
     op->pdl = op->fused_grid > 0 && !(env && env[0] == '0');
   }
   if (m->P > 1 && comm) {
@@ -1289,67 +1285,6 @@ int finish_result(hb_op* op, int32_t iters, double* rr_hist_host, hb_cg_result* 
   return HB_OK;
 }
 
-// ---- fused-p CG (variant 2, P = 1 fixed mode): iteration j =
-//   operator (ASM == 3): p_j = r_j + beta_j p_{j-1} formed in the gather, stored once per DOF,
-//                        Ap_j accumulated into a zeroed Ap, p_j.Ap_j as element energy
-//   cg_update_xrz:       alpha, x += alpha p_j, r -= alpha Ap_j, Ap = 0, r.r, beta_{j+1}
-// p_j and p_{j-1} alternate between two buffers (the gather of p_{j-1} and the store of p_j
-// overlap in time).  Two kernels per iteration and no grid barrier; 96 N_G + 52 N_L bytes.
-bool fp_eligible(const hb_op* op) {
-  return op->fusedp && op->variant == 2 && !op->comm && op->sz.P == 1 && !op->jacobi && !op->scat_mode;
-}
-
-int fp_iteration(hb_op* op, double* x, int32_t j, cudaStream_t st) {
-  const int64_t n = op->sz.n_owned;
-  double* P0 = op->p.as<double>();
-  double* P1 = op->p_alt.as<double>();
-  double* pn = (j & 1) ? P1 : P0;
-  op->fp_pold = (j & 1) ? P0 : P1;
-  op->fp_pnew = pn;
-  const int ls = launch_ax(op, op->ax_fp, 0, op->sz.E_local, op->r.as<double>(), op->Ap.as<double>(), st, true, true);
-  op->fp_pold = nullptr;
-  op->fp_pnew = nullptr;
-  HB_TRY(ls);
-  HB_TRY(phase_event(op, op->t_xr, true, st));
-  double* xp = x;
-  const double* pp = pn;
-  double* rp = op->r.as<double>();
-  double* ap = op->Ap.as<double>();
-  int64_t nn = n;
-  const double* ep = op->e_part.as<double>();
-  int nep = op->last_grid;
-  double* rrp = op->partials.as<double>();
-  hbk::CgScalars* s = op->scal.as<hbk::CgScalars>();
-  double* hp = op->hist.as<double>();
-  void* args[] = {&xp, &pp, &rp, &ap, &nn, &ep, &nep, &rrp, &s, &hp};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(op->fused_grid > 0 ? op->fused_grid : vec_grid(std::max<int64_t>(n, 1)));
-  cfg.blockDim = dim3(hbk::VEC_BLOCK);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = op->pdl ? 1 : 0;
-  CU_TRY(cudaLaunchKernelExC(&cfg, (const void*)&hbk::cg_update_xrz, args));
-  op->launches++;
-  HB_TRY(phase_event(op, op->t_xr, false, st));
-  op->last_timed = false;
-  return HB_OK;
-}
-
-int fp_init(hb_op* op, const double* b, double* x, cudaStream_t st) {
-  const int64_t n = op->sz.n_owned;
-  // r = b, p_{-1} = b (any finite value: beta_0 = 0), x = 0, Ap = 0, r.r
-  hbk::cg_init<<<vec_grid(2 * std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
-      b, x, op->r.as<double>(), op->p_alt.as<double>(), op->Ap.as<double>(), n, 0.0, op->partials.as<double>(),
-      op->scal.as<hbk::CgScalars>(), nullptr, nullptr);
-  op->launches++;
-  CU_TRY(cudaGetLastError());
-  CU_TRY(cudaMemsetAsync(&op->scal.as<hbk::CgScalars>()->beta, 0, sizeof(double), st));
-  return HB_OK;
-}
-
 int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_host, hb_cg_result* res,
              cudaStream_t st) {
   HB_TRY(ensure_hist(op, K));
@@ -1367,9 +1302,8 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
     cudaGraph_t graph;
     cudaStream_t cs = op->cap_stream;
     CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    const bool fp = fp_eligible(op);
-    int status = fp ? fp_init(op, b, x, cs) : cg_init(op, b, x, cs);
-    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = fp ? fp_iteration(op, x, j, cs) : cg_iteration(op, x, cs);
+    int status = cg_init(op, b, x, cs);
+    for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
     cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
     CU_TRY(ce);
@@ -1516,8 +1450,7 @@ extern "C" int hb_cg_solve(hb_op* op, const double* b, double* x, int32_t max_it
   HB_TRY(check_multi(op, "hb_cg_solve"));
   cudaStream_t st = (cudaStream_t)stream;
   if (eps < 0) return cg_fixed(op, b, x, max_iters, rr_hist_host, res, st);
-  const char* env = getenv("HB_TOL_GRAPH");
-  if (op->fused_grid > 0 && !(env && env[0] == '0')) return cg_tol_graph(op, b, x, max_iters, eps, rr_hist_host, res, st);
+  if (op->fused_grid > 0 && op->tol_device_loop) return cg_tol_graph(op, b, x, max_iters, eps, rr_hist_host, res, st);
   return cg_tol(op, b, x, max_iters, eps, rr_hist_host, res, st);
 }
 
@@ -1538,41 +1471,6 @@ extern "C" int hb_cg_solve_host(hb_op* op, const double* b_host, double* x_host,
 
 // CSR of Z^T over owned DOFs, slots in ascending (e, n) order (counting sort by gid), and the
 // y_L buffer -- shared by the deterministic variant and the scattered-storage CG
-// designated slot of every DOF: the first slot (e, n) referencing it
-__global__ void des_first_kernel(const int32_t* __restrict__ idx, int64_t NL, int32_t* first) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < NL; t += (int64_t)gridDim.x * blockDim.x)
-    atomicMin(first + idx[t], (int32_t)t);
-}
-__global__ void des_mark_kernel(const int32_t* __restrict__ idx, int64_t NL, const int32_t* __restrict__ first,
-                                int32_t* out) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < NL; t += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t g = idx[t];
-    out[t] = first[g] == (int32_t)t ? (int32_t)((uint32_t)g | 0x80000000u) : g;
-  }
-}
-
-static int setup_fusedp(hb_op* op, cudaStream_t st) {
-  if (op->fusedp) return HB_OK;
-  const int64_t NL = op->sz.N_L, n = op->sz.n_owned;
-  if (NL >= INT32_MAX) { set_error("fused-p variant: more than 2^31 slots on one rank"); return HB_ERR_ARG; }
-  HB_TRY(op->idx_des.alloc(NL * 4));
-  HB_TRY(op->p_alt.alloc(std::max<int64_t>(n, 1) * 8));
-  if (NL > 0) {
-    DevBuf first;
-    HB_TRY(first.alloc(n * 4));
-    CU_TRY(cudaMemsetAsync(first.p, 0x7f, n * 4, st));
-    des_first_kernel<<<num_sms() * 8, 256, 0, st>>>(op->idx.as<int32_t>(), NL, first.as<int32_t>());
-    des_mark_kernel<<<num_sms() * 8, 256, 0, st>>>(op->idx.as<int32_t>(), NL, first.as<int32_t>(), op->idx_des.as<int32_t>());
-    CU_TRY(cudaGetLastError());
-    CU_TRY(cudaStreamSynchronize(st));
-  }
-  op->ax_fp = pick_ax(op->N, false, op->mass_mode == 1, 3);
-  HB_TRY(prepare_kernel(op->ax_fp));
-  if ((size_t)op->ax_fp.grid_max * 8 + 64 > op->e_part.bytes) HB_TRY(op->e_part.alloc((size_t)op->ax_fp.grid_max * 8 + 64));
-  op->fusedp = true;
-  return HB_OK;
-}
-
 static int ensure_csr(hb_op* op) {
   if (op->yL.p) return HB_OK;
   const int64_t n = op->sz.n_owned, NL = op->sz.N_L;
@@ -1592,13 +1490,12 @@ static int ensure_csr(hb_op* op) {
 }
 
 extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
-  if (!op || variant < 0 || variant > 2) { set_error("hb_op_set_variant: bad argument"); return HB_ERR_ARG; }
+  if (!op || variant < 0 || variant > 1) { set_error("hb_op_set_variant: bad argument"); return HB_ERR_ARG; }
   if (variant >= 1 && (op->sz.P > 1 || op->comm)) {
-    set_error("hb_op_set_variant: variants 1 and 2 are available for P = 1 only");
+    set_error("hb_op_set_variant: variant 1 is available for P = 1 only");
     return HB_ERR_STATE;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (variant == 2) HB_TRY(setup_fusedp(op, st));
   if (variant == 1) {
     HB_TRY(ensure_csr(op));
     if (!op->ax_yl.fn) {
@@ -1772,6 +1669,21 @@ extern "C" int hb_op_jacobi_diagonal(hb_op* op, double* diag_dev, void* stream) 
   CU_TRY(cudaMemcpyAsync(diag_dev, op->invd.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   hbk::invert_kernel<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(diag_dev, n, 0.0);
   CU_TRY(cudaGetLastError());
+  return HB_OK;
+}
+
+extern "C" int hb_op_set_tolerance_loop(hb_op* op, int device) {
+  if (!op || (device != 0 && device != 1)) { set_error("hb_op_set_tolerance_loop: bad argument"); return HB_ERR_ARG; }
+  op->tol_device_loop = device == 1;
+  return HB_OK;
+}
+
+extern "C" int hb_op_launch_shape(const hb_op* op, int32_t out[4]) {
+  if (!op || !out) { set_error("hb_op_launch_shape: null pointer"); return HB_ERR_ARG; }
+  out[0] = op->ax_plain.grid_max;
+  out[1] = op->ax_plain.block;
+  out[2] = op->ax_plain.epb;
+  out[3] = (int32_t)op->ax_plain.smem;
   return HB_OK;
 }
 

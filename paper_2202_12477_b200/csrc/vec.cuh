@@ -460,62 +460,6 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
   }
 }
 
-// Fused-p CG (P = 1, operator ASM == 3): the operator of iteration j formed p_j (designated
-// slots) and Ap_j (zero-initialised); this single pass does
-//   pAp = sum of the operator's energy partials (identical in every CTA, fixed order)
-//   alpha = r.r / pAp;  x += alpha p_j;  r -= alpha Ap_j;  Ap = 0;  r.r partials
-// and the last CTA publishes r_{j+1}.r_{j+1}, beta_{j+1} = r_{j+1}.r_{j+1} / r_j.r_j (c15
-// guards) and the history -- no grid barrier (the p update lives in the next operator).
-__global__ void __launch_bounds__(VEC_BLOCK)
-cg_update_xrz(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
-              int64_t n, const double* __restrict__ e_part, int n_epart, double* rr_part, CgScalars* s,
-              double* hist) {
-  __shared__ double s_b;
-  pdl_wait();
-  double ev = 0.0;
-  for (int b = threadIdx.x; b < n_epart; b += VEC_BLOCK) ev += e_part[b];
-  ev = block_sum(ev);
-  if (threadIdx.x == 0) s_b = ev;
-  __syncthreads();
-  const double pAp = s_b;
-  const double rr = s->rr_new;  // r_j.r_j
-  const double alpha = (pAp != 0.0) ? rr / pAp : 0.0;  // c15 guard
-  const int64_t n2 = n >> 1;
-  const int64_t stride = (int64_t)gridDim.x * VEC_BLOCK;
-  double acc = 0.0;
-  {
-    double2* x2 = reinterpret_cast<double2*>(x);
-    double2* r2 = reinterpret_cast<double2*>(r);
-    const double2* p2 = reinterpret_cast<const double2*>(p);
-    double2* a2 = reinterpret_cast<double2*>(Ap);
-    for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += stride) {
-      double2 xv = x2[l], pv = p2[l], rv = r2[l], av = a2[l];
-      xv.x = fma(alpha, pv.x, xv.x); xv.y = fma(alpha, pv.y, xv.y);
-      rv.x = fma(-alpha, av.x, rv.x); rv.y = fma(-alpha, av.y, rv.y);
-      x2[l] = xv; r2[l] = rv;
-      a2[l] = make_double2(0.0, 0.0);
-      acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
-    }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-      const int64_t l = n - 1;
-      x[l] = fma(alpha, p[l], x[l]);
-      const double rv = fma(-alpha, Ap[l], r[l]);
-      r[l] = rv;
-      Ap[l] = 0.0;
-      acc = fma(rv, rv, acc);
-    }
-  }
-  double rr_new;
-  if (finish_reduction(acc, rr_part, &s->ticket, &rr_new)) {
-    s->pAp = pAp;
-    s->rr = rr;
-    if (hist) hist[s->it] = rr;
-    s->rr_new = rr_new;
-    s->beta = (rr != 0.0) ? rr_new / rr : 0.0;  // c15 guard
-    s->it += 1;
-  }
-}
-
 // Split form used with P > 1: r -= alpha Ap with r.r first, so the r.r allreduce can
 // run on the communication stream while x += alpha p executes ("hidden behind the AXPY").
 __global__ void __launch_bounds__(VEC_BLOCK)

@@ -92,6 +92,8 @@ _SIGS = {
     "hb_op_set_profiling": (C.c_int, [_p, C.c_int]),
     "hb_op_set_jacobi": (C.c_int, [_p, C.c_int, _p]),
     "hb_op_set_variant": (C.c_int, [_p, C.c_int, _p]),
+    "hb_op_set_tolerance_loop": (C.c_int, [_p, C.c_int]),
+    "hb_op_launch_shape": (C.c_int, [_p, _i32p]),
     "hb_op_jacobi_diagonal": (C.c_int, [_p, _p, _p]),
     "hb_op_kernel_time": (C.c_int, [_p, _i64p, _dp]),
     "hb_op_launch_count": (C.c_int, [_p, _i64p]),
@@ -344,9 +346,18 @@ class Operator:
         return res.iterations, (h[:res.iterations + 1].copy() if hist else None)
 
     def set_variant(self, variant: int, stream=None):
-        """0: fused scatter-add (default); 1: y_L + deterministic CSR gather (P = 1);
-        2: fused p update -- the CG p update runs inside the next operator (P = 1, fixed mode)."""
+        """0: fused scatter-add (default); 1: y_L + deterministic CSR gather (P = 1)."""
         _check(_lib.hb_op_set_variant(self._h, int(variant), _stream(stream)))
+
+    def set_tolerance_loop(self, device: bool):
+        """Tolerance-mode CG loop: on the device (one graph, WHILE node; default) or host-driven."""
+        _check(_lib.hb_op_set_tolerance_loop(self._h, int(bool(device))))
+
+    def launch_shape(self) -> dict:
+        """Operator launch shape: resident grid, threads per CTA, elements per CTA, shared bytes."""
+        a = np.zeros(4, dtype=np.int32)
+        _check(_lib.hb_op_launch_shape(self._h, _ptr(a, C.c_int32)))
+        return {"grid": int(a[0]), "block": int(a[1]), "epb": int(a[2]), "smem": int(a[3])}
 
     def set_jacobi(self, enable: bool, stream=None):
         """Jacobi-preconditioned CG for subsequent cg() calls (P = 1)."""

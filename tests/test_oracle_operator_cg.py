@@ -251,3 +251,82 @@ def test_diagonal_and_pcg(mass_mode):
     assert np.max(np.abs(xp - xd)) <= 1e-9 * np.max(np.abs(xd))
     if mass_mode == 1:
         assert jp < jc
+
+
+# ---------------------------------------------------------------- pins of the parity checkers
+# apply_abs_explicit / apply_abs give the c17 error scale s (|y_i - o_i| <= 1e-12 s_i) and
+# apply_entries the sampled full-size ground truth; each is pinned to something other than
+# itself (dense brute force, exact identities, the pinned apply()).
+
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_abs_explicit_single_element_equals_dense(N):
+    """One element: no cross-element sums, so s = |A| |x| exactly with the dense A."""
+    x, w, D, gid, G, M, NG = setup((1, 1, 1), N)
+    Gr = random_spd_factors(1, (N + 1) ** 3, seed=40 + N)
+    Mr = random_positive(gid.shape, seed=41)
+    A = operator.dense(gid, NG, D, Gr, 0.8, Mr)
+    xv = uniform_vector(NG, 42)
+    s = operator.apply_abs_explicit(xv, gid, D, Gr, 0.8, Mr)
+    np.testing.assert_allclose(s, np.abs(A) @ np.abs(xv), rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4])
+@pytest.mark.parametrize("geom", ["box", "random"])
+def test_abs_explicit_bounds_dense_and_is_elementwise(N, geom):
+    """Several elements: s >= |A| |x| entrywise (triangle inequality over the elements sharing
+    a node), with equality at element-interior nodes (one contributing slot); s is the sum of
+    the single-element scales (assembly is additive)."""
+    box = (2, 2, 1)
+    x, w, D, gid, G, M, NG = setup(box, N)
+    Gr = G if geom == "box" else random_spd_factors(gid.shape[0], (N + 1) ** 3, seed=50 + N)
+    A = operator.dense(gid, NG, D, Gr, 1.0, M)
+    xv = uniform_vector(NG, 43)
+    s = operator.apply_abs_explicit(xv, gid, D, Gr, 1.0, M)
+    lower = np.abs(A) @ np.abs(xv)
+    assert np.all(s >= lower * (1 - 1e-14))
+    counts = np.bincount(gid.ravel(), minlength=NG)
+    one = counts == 1
+    np.testing.assert_allclose(s[one], lower[one], rtol=1e-13, atol=0)
+    parts = sum(operator.apply_abs_explicit(xv, gid[e:e + 1], D, Gr[e:e + 1], 1.0, M[e:e + 1])
+                for e in range(gid.shape[0]))
+    np.testing.assert_allclose(s, parts, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("geom", ["box", "random"])
+def test_abs_sumfactorised_bounds_explicit(N, geom):
+    """apply_abs (used as the c17 scale for N > 5) is |D|^T |G| |D| sum-factorised: it equals
+    apply() run on |x| with |D|, |G|, |lambda|, |M| (an identity of the sum-factorisation,
+    with apply() pinned above), is >= the explicit |S_e||u| scale, and at most 10x it (the
+    looseness of the bound, reading R5: measured max 4.1x at N <= 6, 8.0x at N = 15)."""
+    box = (2, 2, 1)
+    x, w, D, gid, G, M, NG = setup(box, N)
+    Gr = G if geom == "box" else random_spd_factors(gid.shape[0], (N + 1) ** 3, seed=60 + N)
+    Mr = random_positive(gid.shape, seed=61)
+    xv = uniform_vector(NG, 44)
+    s1 = operator.apply_abs(xv, gid, D, Gr, -0.9, Mr)
+    np.testing.assert_allclose(s1, operator.apply(np.abs(xv), gid, np.abs(D), np.abs(Gr), 0.9, Mr),
+                               rtol=1e-14, atol=0)
+    s2 = operator.apply_abs_explicit(xv, gid, D, Gr, -0.9, Mr)
+    assert np.all(s1 >= s2 * (1 - 1e-14))
+    assert np.all(s1 <= 10.0 * s2)
+
+
+@pytest.mark.parametrize("N,mass_mode", [(3, 0), (4, 1), (2, 0)])
+def test_apply_entries_equals_apply(N, mass_mode):
+    """apply_entries (full-size sampled ground truth) equals the pinned apply() at EVERY gid
+    of a small mesh (corners, edges, faces, interiors), random SPD G, both mass modes."""
+    box = (3, 2, 2)
+    x, w, D, gid, G, M, NG = setup(box, N, mass_mode=mass_mode)
+    Gr = random_spd_factors(gid.shape[0], (N + 1) ** 3, seed=70 + N)
+    if mass_mode == 1:
+        M = random_positive(gid.shape, seed=71)
+    xv = uniform_vector(NG, 72)
+    ref = operator.apply(xv, gid, D, Gr, 1.3, M)
+    out = operator.apply_entries(lambda row: xv[row], list(range(NG)), *box, N, D, lambda e: Gr[e], 1.3,
+                                 lambda e, row: M[e], mesh.l2g)
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+    # with |.| inputs it gives the sum-factorised scale (the full-size test's c17 scale)
+    sabs = operator.apply_entries(lambda row: np.abs(xv[row]), list(range(NG)), *box, N, np.abs(D),
+                                  lambda e: np.abs(Gr[e]), 1.3, lambda e, row: M[e], mesh.l2g)
+    np.testing.assert_allclose(sabs, operator.apply_abs(xv, gid, D, Gr, 1.3, M), rtol=1e-13, atol=0)
