@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--no-profile", action="store_true", help="do not bracket operator launches with events")
+    ap.add_argument("--no-profile", action="store_true", help="skip the operator-share pass (no roofline)")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 N=7 operator roofline block")
     ap.add_argument("--variant", type=int, default=0, help="0 fused scatter-add, 1 y_L + CSR (P=1), 2 fused p update (P=1)")
     ap.add_argument("--jacobi", action="store_true", help="Jacobi-preconditioned CG (P=1; not the NekBone FOM)")
     ap.add_argument("--storage", default="assembled", choices=["assembled", "scattered"],
@@ -266,6 +267,50 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def c3_operator_roofline(hb, ledger, peak, peak_src, device_index, reps=50, rounds=5):
+    """C3 at N=7 (52^3 elements, 48.6 M DOFs, BASELINE configs[2]) operator roofline by the
+    paper's method (c24): `reps` back-to-back hb_op_apply calls after warm-up, the
+    operator kernel bracketed by CUDA events on its stream (outside any graph), the mean per
+    round, the median of `rounds` rounds; clocks sampled during the rounds."""
+    import torch
+    box, N = (52, 52, 52), 7
+    m = hb.Mesh(*box, N)
+    op = hb.Operator(m)
+    n = op.n_owned
+    s = m.sizes
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    op.forcing(2, x)
+    y = torch.empty_like(x)
+    for _ in range(5):
+        op.apply(x, y)
+    torch.cuda.synchronize()
+    means = []
+    with ClockSampler(device_index) as clk:
+        for _ in range(rounds):
+            op.set_profiling(True)
+            for _ in range(reps):
+                op.apply(x, y)
+            torch.cuda.synchronize()
+            nl, t = op.kernel_time()
+            means.append(t)
+    op.set_profiling(False)
+    med = sorted(means)[len(means) // 2]
+    alg = ledger.op_bytes_fused(n, s["N_L"], 0)
+    achieved = alg / med / 1e9
+    out = {"workload": "C3 N=7: E=52x52x52 box, 48.6 M DOFs, operator apply (mass mode 0, lambda = 1)",
+           "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 4), "peak_source": peak_src,
+           "launch_ms": round(med * 1e3, 4), "round_means_ms": [round(v * 1e3, 4) for v in means],
+           "timing": f"median of {rounds} means of {reps} back-to-back applies (P:268, c24), kernel events",
+           "alg_bytes_per_launch": alg,
+           "paper_ledger_gbs": round(ledger.op_bytes_paper(n, s["N_L"]) / med / 1e9, 1),
+           "op_gflops": round(ledger.op_flops(s["E_local"], N) / med / 1e9, 1),
+           "clocks": clk.summary()}
+    del op, m
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -342,54 +387,66 @@ def main():
         else:
             op.cg(b, x, K)
 
-    if not args.no_profile:
-        # events around every 10th operator launch (inside the CG graph): live kernel timing
-        # over the timed region at negligible overhead
-        # (P > 1: every launch -- an apply is three launches, A / halo / B, of different sizes)
-        op.set_profiling(True, stride=10 if world == 1 else 1)
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # ---- timed region: K steps, device-timed with events, L2 flushed between steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    op_times = []
-    phases = []
-    l0 = op.launch_count()
-    with ClockSampler(local_rank) as clk:
+    def timed_steps(nsteps):
+        """nsteps CG steps, each bracketed by CUDA events on the launching stream, L2 flushed
+        (256 MiB write) before each; returns the mean step time in ms (this rank)."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nsteps)]
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        for t in range(args.steps):
+        for t in range(nsteps):
             flush.zero_()
             ev[t][0].record(stream)
             step()
             ev[t][1].record(stream)
-            if not args.no_profile:
-                op_times.append(op.kernel_time())  # synchronises on this step's last op event
-                phases.append(op.phase_times())
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    launches = op.launch_count() - l0
-    step_ms = [a.elapsed_time(bv) for a, bv in ev]
-    my_ms = sum(step_ms) / len(step_ms)
+        return sum(a.elapsed_time(bv) for a, bv in ev) / nsteps
+
     rdev = "cpu" if ipc else "cuda"
-    tmax = torch.tensor([my_ms], dtype=torch.float64, device=rdev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ms = tmax.item()
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=rdev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    # ---- timed region: K steps, no instrumentation inside the solve
+    l0 = op.launch_count()
+    with ClockSampler(local_rank) as clk:
+        my_ms = timed_steps(args.steps)
+    launches = op.launch_count() - l0
+    ms = max_over_ranks(my_ms)
     fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (ms * 1e-3) / 1e9
     gdofs = NG * K / (ms * 1e-3) / 1e9
+
+    # ---- the operator's share of a step, without instrumenting the solve: the same graph with
+    # the operator launches removed (vector kernels only, hb_op_set_timing_mode) timed the same
+    # way; (step - vector-only step) / K = the operator's in-situ time per iteration, an upper
+    # bound (alone, the vector kernels find their vectors in L2), so the fraction below is a
+    # lower bound
+    vec_ms = None
+    if args.storage == "assembled" and not args.no_profile:
+        op.set_timing_mode(True)
+        for _ in range(2):
+            step()
+        vec_ms = max_over_ranks(timed_steps(args.steps))
+        op.set_timing_mode(False)
+        step()  # restore x / the solver state (and re-validate the normal graph)
+        torch.cuda.synchronize()
 
     # ---- end-to-end: same solve through the host-buffer C-ABI call (H2D + D2H inside)
     bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     bh.copy_(b.cpu())
     xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     bnp, xnp = bh.numpy(), xh.numpy()
-    op.set_profiling(False)
     for _ in range(2 if args.storage == "assembled" else 0):
         op.cg_host(bnp, xnp, K, hist=False)
     torch.cuda.synchronize()
@@ -402,20 +459,15 @@ def main():
         t0 = time.perf_counter()
         op.cg_host(bnp, xnp, K, hist=False)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_t = torch.tensor([sum(e2e_ms) / max(len(e2e_ms), 1)], dtype=torch.float64, device=rdev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (e2e_t.item() * 1e-3) / 1e9 if e2e_ms else None
+    e2e_v = max_over_ranks(sum(e2e_ms) / max(len(e2e_ms), 1))
+    e2e_fom = ledger.nekbone_flops_per_iter(E_glob, N) * K / (e2e_v * 1e-3) / 1e9 if e2e_ms else None
 
-    # ---- roofline of the dominant kernel (operator), from the live event timings
+    # ---- roofline of the dominant kernel (operator)
     peak, peak_src = peaks()
     roof = None
     roof_apply_s = None
-    if op_times:
-        n_l = sum(c for c, _ in op_times)
-        mean_s = sum(c * t for c, t in op_times) / max(n_l, 1)
-        if world > 1:  # kernel time of one whole apply = all timed launches of a step / K applies
-            mean_s = sum(c * t for c, t in op_times) / (len(op_times) * K)
+    if vec_ms is not None:
+        mean_s = (ms - vec_ms) * 1e-3 / K
         alg_bytes = ledger.op_bytes_fused(n, NL_loc, 0)
         achieved = alg_bytes / mean_s / 1e9
         roof_apply_s = mean_s
@@ -435,8 +487,9 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "frac_of_datasheet_7700": round(achieved / 7700.0, 4),
                 "frac_of_stream8to1": round(achieved / s81, 4) if s81 else None,
-                "kernel": f"ax_lines<N={N}>" + (" (A + halo + B launches of one apply, summed)" if world > 1 else ""),
-                "launch_ms": round(mean_s * 1e3, 4), "launches_timed": n_l,
+                "kernel": f"operator N={N}" + (" (A + halo + B launches and exchanges of one apply)" if world > 1 else ""),
+                "launch_ms": round(mean_s * 1e3, 4),
+                "timing": "in-situ share: (CG step - same step without operator launches) / iterations, CUDA events",
                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                 "paper_ledger_gbs": round(ledger.op_bytes_paper(n, NL_loc) / mean_s / 1e9, 1),
                 "op_gflops": round(ledger.op_flops(s["E_local"], N) / mean_s / 1e9, 1)}
@@ -449,6 +502,10 @@ def main():
         ko, kv = f"N{N}_{blk[0]}x{blk[1]}x{blk[2]}", f"vec_N{N}_{blk[0]}x{blk[1]}x{blk[2]}"
         if ko in dbl and kv in dbl:
             measured_bpd = round((dbl[ko] + dbl[kv]) / NG, 2)
+
+    roof_c3 = None
+    if world == 1 and not args.no_c3 and (tuple(blk), N) == ((16, 16, 16), 7):
+        roof_c3 = c3_operator_roofline(hb, ledger, peak, peak_src, local_rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -483,12 +540,11 @@ def main():
                "e2e": ({"value": round(e2e_fom, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
                         "d2h_bytes_per_step": 8 * n + 48} if e2e_ms else None),
                "gpu_launches": launches,
-               "phase_ms_per_iter": ({"operator": round(1e3 * (roof_apply_s if roof_apply_s else
-                                                              sum(p[0] for p in phases) / len(phases)), 4),
-                                      "xr_update": round(1e3 * sum(p[1] for p in phases) / len(phases), 4),
-                                      "p_update": round(1e3 * sum(p[2] for p in phases) / len(phases), 4)}
-                                     if phases else None),
+               "phase_ms_per_iter": ({"operator": round(1e3 * roof_apply_s, 5),
+                                      "vector_kernels": round(vec_ms / K, 5),
+                                      "sum": round(ms / K, 5)} if vec_ms is not None else None),
                "roofline": roof,
+               "roofline_c3": roof_c3,
                "cpu_baseline": cpu,
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)

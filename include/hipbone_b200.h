@@ -213,6 +213,13 @@ int hb_op_jacobi_diagonal(hb_op* op, double* diag_dev, void* stream);
  * device inside one CUDA graph (WHILE conditional node); device = 0 runs a host-driven loop that
  * reads r.r back every iteration (the reference behaviour for tests).  HB_ERR_ARG otherwise. */
 int hb_op_set_tolerance_loop(hb_op* op, int device);
+/* Measurement hook for splitting a fixed-mode CG step into its kernels without instrumenting
+ * it: mode = 1 makes subsequent fixed-mode hb_cg_solve calls run the same graph WITHOUT the
+ * operator launches (vector kernels only; x and the history are meaningless), so that
+ * (t(mode 0) - t(mode 1)) / iterations is the operator's in-situ share of an iteration
+ * (an upper bound: the vector kernels alone find their vectors in L2).  mode = 0 restores
+ * the solver.  HB_ERR_ARG otherwise. */
+int hb_op_set_timing_mode(hb_op* op, int mode);
 /* Launch shape of the operator kernel used by hb_op_apply / hb_cg_solve on the rank's
  * interior elements: out[0] = resident grid (CTAs the kernel launches at most; it loops over
  * elements beyond that), out[1] = threads per CTA, out[2] = elements per CTA per loop trip,

@@ -304,6 +304,7 @@ struct hb_op {
   DevBuf r, p, Ap, xs, partials, e_part, pp_part, rz_part, invd, scal, hist, dot_out, dot_ticket;
   bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
   bool tol_device_loop = true;  // tolerance mode as one graph with a WHILE node (P = 1)
+  bool timing_vec_only = false; // measurement hook: fixed-mode CG without the operator launches
   int variant = 0;      // 0: fused scatter-add (fp64 RED); 1: y_L + CSR gather (deterministic), P = 1
   DevBuf yL, csr_ptr, csr_slots;
   // NekBone scattered storage (NEXT #4): local vectors of length N_L and the weights W
@@ -339,9 +340,9 @@ struct hb_op {
   int64_t launches = 0;
   // fixed-mode graph cache
   struct GraphKey {
-    int32_t K; const double* b; double* x; bool prof; cudaStream_t st;
+    int32_t K; const double* b; double* x; bool prof; bool vec_only; cudaStream_t st;
     bool operator<(const GraphKey& o) const {
-      return std::tie(K, b, x, prof, st) < std::tie(o.K, o.b, o.x, o.prof, o.st);
+      return std::tie(K, b, x, prof, vec_only, st) < std::tie(o.K, o.b, o.x, o.prof, o.vec_only, o.st);
     }
   };
   struct GraphVal { cudaGraphExec_t exec; int64_t launches; size_t prof_events, prof_xr, prof_p; };
@@ -1250,7 +1251,7 @@ int cg_iteration(hb_op* op, double* x, cudaStream_t st) {
     HB_TRY(cg_vec_part2(op, st));
     return ipc_signal_ready(op, st);
   }
-  HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
+  if (!op->timing_vec_only) HB_TRY(apply_internal(op, op->p.as<double>(), op->Ap.as<double>(), false, st, true));
   HB_TRY(cg_vec_part1(op, x, st));
   return cg_vec_part2(op, st);
 }
@@ -1294,7 +1295,7 @@ int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_h
     for (int32_t j = 0; j < K; ++j) HB_TRY(cg_iteration(op, x, st));
     return finish_result(op, K, rr_hist_host, res, st);
   }
-  hb_op::GraphKey key{K, b, x, op->profiling, st};
+  hb_op::GraphKey key{K, b, x, op->profiling, op->timing_vec_only, st};
   auto it = op->graphs.find(key);
   if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }  // a profiling graph records into events 0..n-1
   if (it == op->graphs.end()) {
@@ -1675,6 +1676,12 @@ extern "C" int hb_op_jacobi_diagonal(hb_op* op, double* diag_dev, void* stream) 
 extern "C" int hb_op_set_tolerance_loop(hb_op* op, int device) {
   if (!op || (device != 0 && device != 1)) { set_error("hb_op_set_tolerance_loop: bad argument"); return HB_ERR_ARG; }
   op->tol_device_loop = device == 1;
+  return HB_OK;
+}
+
+extern "C" int hb_op_set_timing_mode(hb_op* op, int mode) {
+  if (!op || (mode != 0 && mode != 1)) { set_error("hb_op_set_timing_mode: bad argument"); return HB_ERR_ARG; }
+  op->timing_vec_only = mode == 1;
   return HB_OK;
 }
 

@@ -94,6 +94,7 @@ _SIGS = {
     "hb_op_set_variant": (C.c_int, [_p, C.c_int, _p]),
     "hb_op_set_tolerance_loop": (C.c_int, [_p, C.c_int]),
     "hb_op_launch_shape": (C.c_int, [_p, _i32p]),
+    "hb_op_set_timing_mode": (C.c_int, [_p, C.c_int]),
     "hb_op_jacobi_diagonal": (C.c_int, [_p, _p, _p]),
     "hb_op_kernel_time": (C.c_int, [_p, _i64p, _dp]),
     "hb_op_launch_count": (C.c_int, [_p, _i64p]),
@@ -352,6 +353,10 @@ class Operator:
     def set_tolerance_loop(self, device: bool):
         """Tolerance-mode CG loop: on the device (one graph, WHILE node; default) or host-driven."""
         _check(_lib.hb_op_set_tolerance_loop(self._h, int(bool(device))))
+
+    def set_timing_mode(self, vec_only: bool):
+        """Measurement hook: fixed-mode CG without the operator launches (vector kernels only)."""
+        _check(_lib.hb_op_set_timing_mode(self._h, int(bool(vec_only))))
 
     def launch_shape(self) -> dict:
         """Operator launch shape: resident grid, threads per CTA, elements per CTA, shared bytes."""
