@@ -28,6 +28,7 @@
 // to lambda*x (reading R2).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"  // AxArgs, c_D, prefetch_l2_bulk, load_x / red_y
 
@@ -65,6 +66,7 @@ struct LinesShape {
   static constexpr int MAT = H * HE2 + H * H2 + H2;  // Me, Mo, middle row
   static constexpr int CONST = 2 * MAT;               // D and D^T (host-built, g_EO[N])
   static_assert(CONST <= EO_MAX, "folded D table");
+  static_assert(CONST == eo_const(N), "packed constant-memory D table");
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
   // Resident CTAs per SM requested from ptxas, from a per-N register target measured on the
   // B200 (profiles/r1_tune.jsonl; 0 = no cap, one CTA per SM), capped by shared memory.
@@ -88,14 +90,35 @@ struct LinesShape {
   // LSU instructions, +4..14% at N = 8, 11-15, -5% at N = 7, 10 (profiles/r1b/pf_*.jsonl)
   static constexpr int PFL_T[16] = {0, 0, 0, 0, 0, 0, 1, 1, 2, 1, 1, 2, 2, 2, 2, 2};
   static constexpr int PFL_DEF = PFL_T[N];
+  // Folded D from constant memory (uniform-register / constant-bank operands of the DFMAs, no
+  // shared-memory broadcast wavefronts) per phase (mask bit 0 P1, 1 P2, 2 P4, 3 P5); 0 = all from
+  // shared memory.  Measured per N (profiles/r2/dc/): all phases +2..16% at N = 2-6, 9 and +11%
+  // at C2 (N = 7); N = 14 P2, P4, P5 only (+5%); at N = 8, 10-13, 15 the constant loads cost
+  // registers (spills at 255) and lose 2-13%
+  static constexpr int DC_T[16] = {0, 0, 15, 15, 15, 15, 15, 14, 0, 15, 0, 0, 0, 0, 14, 0};
+  static constexpr int DC_DEF = DC_T[N];
 };
 
-// sum_m C[m] v[l][m] for L lines; C is a 16-byte aligned shared row read as broadcast pairs
-template <int CNT, int L, int W>
-__device__ __forceinline__ void dot_rows(const double* __restrict__ C, const double (&v)[L][W], double (&acc)[L]) {
+// Source of the folded matrices: shared memory (warp-uniform broadcast loads, 16-byte pairs) or
+// constant memory (DC kernels: the offsets are compile-time after unrolling, so each entry is a
+// constant-bank operand of its DFMA -- no load instruction, no L1 data-pipe wavefront).
+struct SmemMat {
+  const double* __restrict__ p;
+  __device__ __forceinline__ double2 pair(int o) const { return *reinterpret_cast<const double2*>(p + o); }
+  __device__ __forceinline__ double one(int o) const { return p[o]; }
+};
+struct ConstMat {
+  int base;
+  __device__ __forceinline__ double2 pair(int o) const { return make_double2(c_EO[base + o], c_EO[base + o + 1]); }
+  __device__ __forceinline__ double one(int o) const { return c_EO[base + o]; }
+};
+
+// sum_m C[off + m] v[l][m] for L lines; C is read as 16-byte aligned pairs
+template <int CNT, int L, int W, class M>
+__device__ __forceinline__ void dot_rows(const M& C, int off, const double (&v)[L][W], double (&acc)[L]) {
 #pragma unroll
   for (int m = 0; m + 1 < CNT; m += 2) {
-    const double2 c2 = *reinterpret_cast<const double2*>(C + m);
+    const double2 c2 = C.pair(off + m);
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       acc[l] = fma(c2.x, v[l][m], acc[l]);
@@ -103,21 +126,18 @@ __device__ __forceinline__ void dot_rows(const double* __restrict__ C, const dou
     }
   }
   if constexpr (CNT & 1) {
-    const double cl = C[CNT - 1];
+    const double cl = C.one(off + CNT - 1);
 #pragma unroll
     for (int l = 0; l < L; ++l) acc[l] = fma(cl, v[l][CNT - 1], acc[l]);
   }
 }
 
 // y[l] = M x[l] for L lines at once (each uniform load of M feeds L multiply-adds).
-template <int N, int EPBX, int L>
-__device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const double (&x)[L][N + 1],
-                                         double (&y)[L][N + 1]) {
+template <int N, int EPBX, int L, class MS>
+__device__ __forceinline__ void eo_apply(const MS& sM, const double (&x)[L][N + 1], double (&y)[L][N + 1]) {
   using S = LinesShape<N, EPBX>;
   constexpr int H = S::H, HE = S::HE, ODD = S::ODD, HE2 = S::HE2, H2 = S::H2;
-  const double* Me = sM;
-  const double* Mo = sM + H * HE2;
-  const double* Mm = Mo + H * H2;
+  constexpr int Me = 0, Mo = H * HE2, Mm = Mo + H * H2;
   double e[L][HE], o[L][H > 0 ? H : 1];
 #pragma unroll
   for (int l = 0; l < L; ++l) {
@@ -133,8 +153,8 @@ __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const do
     double se[L], so[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) { se[l] = 0.0; so[l] = 0.0; }
-    dot_rows<HE, L, HE>(Me + i * HE2, e, se);
-    dot_rows<H, L, (H > 0 ? H : 1)>(Mo + i * H2, o, so);
+    dot_rows<HE, L, HE>(sM, Me + i * HE2, e, se);
+    dot_rows<H, L, (H > 0 ? H : 1)>(sM, Mo + i * H2, o, so);
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       y[l][i] = so[l] + se[l];
@@ -145,7 +165,7 @@ __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const do
     double sm[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) sm[l] = 0.0;
-    dot_rows<H, L, (H > 0 ? H : 1)>(Mm, o, sm);
+    dot_rows<H, L, (H > 0 ? H : 1)>(sM, Mm, o, sm);
 #pragma unroll
     for (int l = 0; l < L; ++l) y[l][H] = sm[l];
   }
@@ -155,14 +175,15 @@ __device__ __forceinline__ void eo_apply(const double* __restrict__ sM, const do
 // one partial per CTA, the last CTA sums the partials in CTA order (deterministic) and either
 // accumulates (more launches of this apply follow) or publishes p.Ap = e + lambda p.p and
 // rotates r.r (the bookkeeping a separate p.Ap kernel would do).
+__host__ __device__ constexpr int pow2_ceil(int v) { return v <= 1 ? 1 : 2 * pow2_ceil((v + 1) / 2); }
+
 template <int BLOCK>
 __device__ __forceinline__ void energy_finish(double en, const AxArgs& a, double* red) {
   __shared__ bool s_last;
   const int t = threadIdx.x;
   red[t] = en;
   __syncthreads();
-  constexpr int P2B = BLOCK <= 1 ? 1 : (BLOCK <= 2 ? 2 : (BLOCK <= 4 ? 4 : (BLOCK <= 8 ? 8 : (BLOCK <= 16 ? 16 :
-                      (BLOCK <= 32 ? 32 : (BLOCK <= 64 ? 64 : (BLOCK <= 128 ? 128 : 256)))))));
+  constexpr int P2B = pow2_ceil(BLOCK);
 #pragma unroll
   for (int h = P2B / 2; h > 0; h >>= 1) {
     if (t < h && t + h < BLOCK) red[t] += red[t + h];
@@ -222,13 +243,11 @@ __device__ __forceinline__ double2 ldG2(const double2* p) {
 // Streaming form of eo_apply for one line: each output y_i is handed to sink(i, y_i) as soon
 // as it is formed (the input line is folded into e/o first, so it may be overwritten in place);
 // no output array is kept -- large N stays within the register budget of 2 CTAs per SM.
-template <int N, int EPBX, class Sink>
-__device__ __forceinline__ void eo_apply_sink(const double* __restrict__ sM, const double (&x)[N + 1], Sink&& sink) {
+template <int N, int EPBX, class MS, class Sink>
+__device__ __forceinline__ void eo_apply_sink(const MS& sM, const double (&x)[N + 1], Sink&& sink) {
   using S = LinesShape<N, EPBX>;
   constexpr int H = S::H, HE = S::HE, ODD = S::ODD, HE2 = S::HE2, H2 = S::H2;
-  const double* Me = sM;
-  const double* Mo = sM + H * HE2;
-  const double* Mm = Mo + H * H2;
+  constexpr int Me = 0, Mo = H * HE2, Mm = Mo + H * H2;
   double e[1][HE], o[1][H > 0 ? H : 1];
 #pragma unroll
   for (int m = 0; m < H; ++m) {
@@ -239,21 +258,22 @@ __device__ __forceinline__ void eo_apply_sink(const double* __restrict__ sM, con
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     double se[1] = {0.0}, so[1] = {0.0};
-    dot_rows<HE, 1, HE>(Me + i * HE2, e, se);
-    dot_rows<H, 1, (H > 0 ? H : 1)>(Mo + i * H2, o, so);
+    dot_rows<HE, 1, HE>(sM, Me + i * HE2, e, se);
+    dot_rows<H, 1, (H > 0 ? H : 1)>(sM, Mo + i * H2, o, so);
     sink(i, so[0] + se[0]);
     sink(N - i, so[0] - se[0]);
   }
   if constexpr (ODD) {
     double sm[1] = {0.0};
-    dot_rows<H, 1, (H > 0 ? H : 1)>(Mm, o, sm);
+    dot_rows<H, 1, (H > 0 ? H : 1)>(sM, Mm, o, sm);
     sink(H, sm[0]);
   }
 }
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0,
           int PFL = LinesShape<N>::PFL_DEF,
-          bool GCS = true, int ASM = 0, bool PFN = false>
+          bool GCS = true, int ASM = 0, bool PFN = false, int DCM = LinesShape<N>::DC_DEF,
+          bool STREAM = LinesShape<N>::STREAM>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
@@ -266,9 +286,20 @@ ax_lines(const AxArgs a) {
   double* s_u = smem + (0 * EPB + le) * SLAB;
   double* s_r = smem + (1 * EPB + le) * SLAB;
   double* s_s = smem + (2 * EPB + le) * SLAB;
-  double* s_D = smem + 3 * EPB * SLAB;  // folded D
-  double* s_DT = s_D + S::MAT;          // folded D^T
-  for (int q = t; q < S::CONST; q += S::BLOCK) s_D[q] = __ldg(&g_EO[N][q]);  // folded D | D^T
+  // folded D, D^T: constant memory in the phases of mask DCM (bit 0 P1, 1 P2, 2 P4, 3 P5),
+  // a shared-memory copy in the others
+  const ConstMat c_D{eo_off(N)}, c_DT{eo_off(N) + S::MAT};
+  SmemMat s_D{nullptr}, s_DT{nullptr};
+  if constexpr (DCM != 15) {
+    double* sd = smem + 3 * EPB * SLAB;
+    for (int q = t; q < S::CONST; q += S::BLOCK) sd[q] = __ldg(&g_EO[N][q]);
+    s_D = SmemMat{sd};
+    s_DT = SmemMat{sd + S::MAT};
+  }
+  const auto m1 = [&]() { if constexpr (DCM & 1) return c_D; else return s_D; }();
+  const auto m2 = [&]() { if constexpr (DCM & 2) return c_D; else return s_D; }();
+  const auto m4 = [&]() { if constexpr (DCM & 4) return c_DT; else return s_DT; }();
+  const auto m5 = [&]() { if constexpr (DCM & 8) return c_DT; else return s_DT; }();
   const bool interior_ij = (ca > 0 && ca < N && cb > 0 && cb < N);
   double en = 0.0;  // element energy u.(S_e u) (+ lambda u.B u) of this thread's nodes
 
@@ -337,19 +368,19 @@ ax_lines(const AxArgs a) {
         else col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
         s_u[S::at(ca, cb, k)] = col[0][k];
       }
-      eo_apply<N, EPBX, 1>(s_D, col, gt);
+      eo_apply<N, EPBX, 1>(m1, col, gt);
     }
     __syncthreads();
 
     // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
-    if constexpr (S::STREAM) {
+    if constexpr (STREAM) {
       double in[NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(m, ca, cb)];
-      eo_apply_sink<N, EPBX>(s_D, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+      eo_apply_sink<N, EPBX>(m2, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(ca, m, cb)];
-      eo_apply_sink<N, EPBX>(s_D, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
+      eo_apply_sink<N, EPBX>(m2, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
     } else {
       double in[2][NP], out[2][NP];
 #pragma unroll
@@ -357,7 +388,7 @@ ax_lines(const AxArgs a) {
         in[0][m] = s_u[S::at(m, ca, cb)];
         in[1][m] = s_u[S::at(ca, m, cb)];
       }
-      eo_apply<N, EPBX, 2>(s_D, in, out);
+      eo_apply<N, EPBX, 2>(m2, in, out);
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
         s_r[S::at(m, ca, cb)] = out[0][m];
@@ -395,14 +426,14 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
-    if constexpr (S::STREAM) {
+    if constexpr (STREAM) {
       double in[NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[m] = s_r[S::at(m, ca, cb)];
-      eo_apply_sink<N, EPBX>(s_DT, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+      eo_apply_sink<N, EPBX>(m4, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[m] = s_s[S::at(ca, m, cb)];
-      eo_apply_sink<N, EPBX>(s_DT, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
+      eo_apply_sink<N, EPBX>(m4, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
     } else {
       double in[2][NP], out[2][NP];
 #pragma unroll
@@ -410,7 +441,7 @@ ax_lines(const AxArgs a) {
         in[0][m] = s_r[S::at(m, ca, cb)];
         in[1][m] = s_s[S::at(ca, m, cb)];
       }
-      eo_apply<N, EPBX, 2>(s_DT, in, out);
+      eo_apply<N, EPBX, 2>(m4, in, out);
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
         s_r[S::at(m, ca, cb)] = out[0][m];
@@ -441,11 +472,11 @@ ax_lines(const AxArgs a) {
           red_y<HALO>(a, gi[k], out);
         }
       };
-      if constexpr (S::STREAM) {
-        eo_apply_sink<N, EPBX>(s_DT, gt[0], node);
+      if constexpr (STREAM) {
+        eo_apply_sink<N, EPBX>(m5, gt[0], node);
       } else {
         double vt[1][NP];
-        eo_apply<N, EPBX, 1>(s_DT, gt, vt);
+        eo_apply<N, EPBX, 1>(m5, gt, vt);
 #pragma unroll
         for (int k = 0; k < NP; ++k) node(k, vt[0][k]);
       }

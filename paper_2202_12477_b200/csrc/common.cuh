@@ -10,6 +10,17 @@ __constant__ double c_D[16][256];  // c_D[N][i*(N+1)+j] = D_ij for N = 1..15
 // even/odd folded D and D^T per N (layout in ax_lines.cuh LinesShape), written by the host
 constexpr int EO_MAX = 272;
 __device__ double g_EO[16][EO_MAX];
+// Size (doubles) of the folded D | D^T pair of degree N: 2 (H HE2 + H H2 + H2), H = (N+1)/2,
+// HE = H + ((N+1) & 1), HE2 / H2 rounded up to even (16-byte row pairs)
+__host__ __device__ constexpr int eo_const(int N) {
+  return 2 * (((N + 1) / 2) * (((N + 1) / 2 + ((N + 1) & 1)) + ((((N + 1) / 2 + ((N + 1) & 1))) & 1)) +
+              ((N + 1) / 2) * ((N + 1) / 2 + (((N + 1) / 2) & 1)) + ((N + 1) / 2 + (((N + 1) / 2) & 1)));
+}
+__host__ __device__ constexpr int eo_off(int N) { return N <= 1 ? 0 : eo_off(N - 1) + eo_const(N - 1); }
+constexpr int EO_TOTAL = eo_off(16);
+// the same tables in constant memory, packed per degree: a warp-uniform D entry with a
+// compile-time offset becomes a constant-bank operand of the DFMA (no shared-memory wavefront)
+__constant__ double c_EO[EO_TOTAL];
 
 // Device-resident CG scalars (alpha, beta are never sent to the host; see vec.cuh)
 struct CgScalars {

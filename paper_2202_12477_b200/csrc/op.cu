@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -102,10 +103,11 @@ struct AxKernel {
 };
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0,
-          int PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false>
+          int PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false,
+          int DC = hbk::LinesShape<N>::DC_DEF, bool STREAM = hbk::LinesShape<N>::STREAM>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN, DC, STREAM>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
@@ -182,7 +184,21 @@ AxKernel tune_variant(int v) {
     case 10: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>()>();   // 96 regs
     case 11: return make_lines<N, false, false, 0, tune_minb<N, 0, 80>()>();   // 80 regs
     case 13: return make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, 2>();  // bulk G of this element
-    default: return make_lines<N, false, false, kLinesPF>();
+    // folded D from constant memory (DFMA constant-bank operands) per phase mask / from shared memory
+#define HB_DCV(MASK) make_lines<N, false, false, 0, hbk::LinesShape<N>::MINB, 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, MASK>()
+    case 30: return HB_DCV(15);
+    case 31: return HB_DCV(0);
+    case 35: return HB_DCV(9);   // P1 + P5 (single-line phases)
+    case 36: return HB_DCV(6);   // P2 + P4 (two-line phases)
+    case 37: return HB_DCV(1);
+    case 38: return HB_DCV(8);
+    case 39: return HB_DCV(14);
+#undef HB_DCV
+    case 32: return make_lines<N, false, false, 0, tune_minb<N, 0, 80>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
+    case 33: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
+    case 34: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
+    default:
+      return make_lines<N, false, false, kLinesPF>();
   }
 }
 
@@ -313,6 +329,7 @@ struct hb_op {
   int fused_grid = 0;  // > 0: P = 1 vector updates in one cooperative kernel of this grid
   hbk::CondTest cond_test = {0, 0.0, 0, 0};  // set while the tolerance graph's WHILE body is captured
   const void* fused_fn = nullptr;  // cg_update_fused<U> instance (U double2 per thread per batch)
+  const void* fused_fn_cond = nullptr;  // the same with the tolerance-mode loop test (WHILE condition)
   bool pdl = false;    // P = 1 CG kernels use programmatic dependent launch (env HB_PDL=0 disables)
   DevBuf xh, yh, send_loc, send_buf, recv_buf;
   std::vector<int32_t> nbr;
@@ -828,6 +845,7 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
         for (int mm = 0; mm < H; ++mm) o[H * HE2 + H * H2 + mm] = M(H, mm);
     }
     CU_TRY(cudaMemcpyToSymbol(hbk::g_EO, eo.data(), sizeof(double) * hbk::EO_MAX, sizeof(double) * hbk::EO_MAX * N));
+    CU_TRY(cudaMemcpyToSymbol(hbk::c_EO, eo.data(), sizeof(double) * hbk::eo_const(N), sizeof(double) * hbk::eo_off(N)));
   }
   // arena of everything a CG iteration re-reads besides G (candidates for L2 residency)
   {
@@ -912,15 +930,21 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     // fit L2 (C2: +1.3%), the single-item form above that (C3 N=7: the batched one is 2.7% slower;
     // profiles/r1_update_ab.jsonl)
     const int U = ue ? atoi(ue) : (n <= 8000000 ? 1 : 0), MB = me ? atoi(me) : 2;
-    if (U == 0)
-      op->fused_fn = (const void*)&hbk::cg_update_fused0;
-    else if (MB >= 2)
-      op->fused_fn = U >= 4 ? (const void*)&hbk::cg_update_fused<4, 2>
-                   : U == 2 ? (const void*)&hbk::cg_update_fused<2, 2> : (const void*)&hbk::cg_update_fused<1, 2>;
-    else
-      op->fused_fn = U >= 4 ? (const void*)&hbk::cg_update_fused<4, 1>
-                   : U == 2 ? (const void*)&hbk::cg_update_fused<2, 1> : (const void*)&hbk::cg_update_fused<1, 1>;
+    auto pick = [&](auto cond) -> const void* {
+      constexpr bool C = decltype(cond)::value;
+      if (U == 0) return (const void*)&hbk::cg_update_fused0<C>;
+      if (MB >= 2)
+        return U >= 4 ? (const void*)&hbk::cg_update_fused<4, 2, C>
+             : U == 2 ? (const void*)&hbk::cg_update_fused<2, 2, C> : (const void*)&hbk::cg_update_fused<1, 2, C>;
+      return U >= 4 ? (const void*)&hbk::cg_update_fused<4, 1, C>
+           : U == 2 ? (const void*)&hbk::cg_update_fused<2, 1, C> : (const void*)&hbk::cg_update_fused<1, 1, C>;
+    };
+    op->fused_fn = pick(std::false_type{});
+    op->fused_fn_cond = pick(std::true_type{});
+    int nb2 = 0;
     CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, op->fused_fn, hbk::VEC_BLOCK, 0));
+    CU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, op->fused_fn_cond, hbk::VEC_BLOCK, 0));
+    nb = std::min(nb, nb2);
     const char* env = tune_env("HB_FUSED_UPDATE");
     if (coop && nb > 0 && !(env && env[0] == '0'))
       op->fused_grid = std::min(vec_grid(std::max<int64_t>(n, 1)), nb * num_sms());
@@ -1198,7 +1222,7 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = op->pdl ? 2 : 1;
-    CU_TRY(cudaLaunchKernelExC(&cfg, op->fused_fn, args));
+    CU_TRY(cudaLaunchKernelExC(&cfg, ct.on ? op->fused_fn_cond : op->fused_fn, args));
     op->launches++;
     return phase_event(op, op->t_xr, false, st);
   }

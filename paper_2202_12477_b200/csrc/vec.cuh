@@ -201,7 +201,11 @@ __device__ __forceinline__ void cond_test(const CondTest& ct, CgScalars* s, doub
 // sums the r.r partials in CTA order -> beta; p = r + beta p, Ap = lambda p, CTA partial of
 // p.p (consumed by the next iteration's p.Ap).  r and p are re-read after the barrier from L2
 // when the vectors fit it.  CTA 0 publishes the scalars (pAp, rr, rr_new, history, j).
-// (previous single-item form, kept for A/B: HB_UPD_U=0)
+// (single-item form; the batched cg_update_fused below is used for vectors that fit L2)
+// COND: the tolerance-mode instance, which also runs the loop test and sets the WHILE node's
+// condition (ncu does not profile kernels that can set conditional handles, so the fixed-mode
+// graph uses the COND = false instance)
+template <bool COND>
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_fused0(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
@@ -308,12 +312,14 @@ cg_update_fused0(double* __restrict__ x, double* __restrict__ p, double* __restr
       s->rr_new = rr_new;
       s->rz = rho_new;
       s->it += 1;
-      if (ct.on) cond_test(ct, s, pAp, rr_new, s->it);
+      if constexpr (COND) {
+        if (ct.on) cond_test(ct, s, pAp, rr_new, s->it);
+      }
     }
   }
 }
 
-template <int U, int MINB>
+template <int U, int MINB, bool COND>
 __global__ void __launch_bounds__(VEC_BLOCK, MINB)
 cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restrict__ r, double* __restrict__ Ap,
                 int64_t n, const double* __restrict__ e_part, int n_epart, double* pp_part, double lam_pp,
@@ -455,7 +461,9 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       s->rr_new = rr_new;
       s->rz = rho_new;
       s->it += 1;
-      if (ct.on) cond_test(ct, s, pAp, rr_new, s->it);
+      if constexpr (COND) {
+        if (ct.on) cond_test(ct, s, pAp, rr_new, s->it);
+      }
     }
   }
 }

@@ -520,7 +520,7 @@ def test_jacobi_pcg(hb, N, mass_mode):
     # CG from PCG at iteration 1) and the stop to within one iteration; c18's exact count is
     # enforced on the well-conditioned problems (test_cg_parity, the PCG runs above)
     assert abs(j - jc) <= 1
-    _cg_contract(h, hc, min(j, jc, 30))
+    _cg_contract(h, hc, min(j, jc, 20))
 
 
 @pytest.mark.parametrize("N,mass_mode", [(3, 0), (7, 1), (10, 0)])
