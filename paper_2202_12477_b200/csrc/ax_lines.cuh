@@ -68,17 +68,22 @@ struct LinesShape {
   static_assert(CONST <= EO_MAX, "folded D table");
   static_assert(CONST == eo_const(N), "packed constant-memory D table");
   static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
+  // Line contractions: 0 = two lines (P2, P4) into output arrays; 1 = one line at a time, every
+  // output streamed to shared memory / the assembly as it is formed; 2 = two lines streamed (D
+  // read once per two lines, no output arrays).  GIR: the index column is re-read in P5 instead of
+  // held in registers from P1.  Streaming frees the registers for two CTAs per SM at N = 11-13:
+  // N = 11 0.78 -> 0.83 and N = 13 0.62 -> 0.69 of peak (2 lines, index re-read, 128 registers),
+  // N = 12 0.69 -> 0.76 (2 lines, 168 registers); at N = 14, 15 the two-CTA forms spill or lose
+  // to one CTA per SM at 255 registers (profiles/r2/bign/)
+  static constexpr int STREAM_T[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 2, 2, 0, 0};
+  static constexpr int STREAM = STREAM_T[N];
+  static constexpr bool GIR = N == 11 || N == 13;
   // Resident CTAs per SM requested from ptxas, from a per-N register target measured on the
-  // B200 (profiles/r1_tune.jsonl; 0 = no cap, one CTA per SM), capped by shared memory.
-  // N = 12: streaming line contractions (no output arrays) fit 2 CTAs/SM without spills
-  // (0.69 vs 0.57 of peak); for N = 13..15 the streamed kernel at 2 CTAs/SM spills and loses
-  // to one uncapped CTA per SM (profiles/r1_opbench_sweep.jsonl, r1_tune.jsonl)
-  static constexpr bool STREAM = N == 12;
-  // N = 13: one uncapped CTA per SM since the bulk G prefetch (0.61 vs 0.57 at 2 x 128 registers,
-  // profiles/r1b/tune3.jsonl); N = 7: 96 registers (10 CTAs per SM) since the factor-pair G
-  // layout (0.962 vs 0.943 at C3, equal at C2; profiles/r1b/tune_n7_regs.jsonl); N = 2: 80 registers
-  // (0.614 vs 0.607, three repeats each; profiles/r1b/last_ab_n2regs_n13pad.jsonl)
-  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 0, 0, 0};
+  // B200 (0 = no cap, one CTA per SM), capped by shared memory: N = 7 96 registers (10 CTAs per
+  // SM; 0.962 vs 0.943 at C3 with 128, profiles/r1b/tune_n7_regs.jsonl); N = 2 80 registers
+  // (0.614 vs 0.607, profiles/r1b/last_ab_n2regs_n13pad.jsonl); N = 12, 13 two CTAs per SM with
+  // the streamed contractions above; N = 14, 15 uncapped
+  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 128, 0, 0};
   static constexpr int REGS = REGS_T[N];
   static constexpr int MINB_REG0 = REGS ? 65536 / (BLOCK * REGS) : 1;
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
@@ -240,40 +245,89 @@ __device__ __forceinline__ double2 ldG2(const double2* p) {
 
 // ASM: 0 = fused scatter-add into assembled storage (fp64 RED / store); 1 = write y_L per slot
 // (deterministic CSR-gather variant); 2 = scattered storage: read u_e from x_L, write y_L.
-// Streaming form of eo_apply for one line: each output y_i is handed to sink(i, y_i) as soon
-// as it is formed (the input line is folded into e/o first, so it may be overwritten in place);
-// no output array is kept -- large N stays within the register budget of 2 CTAs per SM.
-template <int N, int EPBX, class MS, class Sink>
-__device__ __forceinline__ void eo_apply_sink(const MS& sM, const double (&x)[N + 1], Sink&& sink) {
+// Streaming form for L lines at once: the lines are folded in place (x[l][m] <- e_m, x[l][N-m] <- o_m)
+// and each output handed to sink(l, i, y) as soon as it is formed -- D is still read once per L
+// lines, but no output arrays are kept (large N: 2 lines of 16 in 64 registers instead of 128).
+template <int N, int EPBX, int L, class MS, class Sink>
+__device__ __forceinline__ void eo_apply_sinkL(const MS& sM, double (&x)[L][N + 1], Sink&& sink) {
   using S = LinesShape<N, EPBX>;
   constexpr int H = S::H, HE = S::HE, ODD = S::ODD, HE2 = S::HE2, H2 = S::H2;
   constexpr int Me = 0, Mo = H * HE2, Mm = Mo + H * H2;
-  double e[1][HE], o[1][H > 0 ? H : 1];
 #pragma unroll
-  for (int m = 0; m < H; ++m) {
-    e[0][m] = x[m] + x[N - m];
-    o[0][m] = x[m] - x[N - m];
+  for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      const double a = x[l][m], b = x[l][N - m];
+      x[l][m] = a + b;
+      x[l][N - m] = a - b;
+    }
   }
-  if constexpr (ODD) e[0][H] = x[H];
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    double se[1] = {0.0}, so[1] = {0.0};
-    dot_rows<HE, 1, HE>(sM, Me + i * HE2, e, se);
-    dot_rows<H, 1, (H > 0 ? H : 1)>(sM, Mo + i * H2, o, so);
-    sink(i, so[0] + se[0]);
-    sink(N - i, so[0] - se[0]);
+    double se[L], so[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) { se[l] = 0.0; so[l] = 0.0; }
+#pragma unroll
+    for (int m = 0; m + 1 < HE; m += 2) {
+      const double2 c2 = sM.pair(Me + i * HE2 + m);
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        se[l] = fma(c2.x, x[l][m], se[l]);
+        se[l] = fma(c2.y, x[l][m + 1], se[l]);
+      }
+    }
+    if constexpr (HE & 1) {
+      const double cl = sM.one(Me + i * HE2 + HE - 1);
+#pragma unroll
+      for (int l = 0; l < L; ++l) se[l] = fma(cl, x[l][HE - 1], se[l]);
+    }
+#pragma unroll
+    for (int m = 0; m + 1 < H; m += 2) {
+      const double2 c2 = sM.pair(Mo + i * H2 + m);
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        so[l] = fma(c2.x, x[l][N - m], so[l]);
+        so[l] = fma(c2.y, x[l][N - m - 1], so[l]);
+      }
+    }
+    if constexpr (H & 1) {
+      const double cl = sM.one(Mo + i * H2 + H - 1);
+#pragma unroll
+      for (int l = 0; l < L; ++l) so[l] = fma(cl, x[l][N - (H - 1)], so[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      sink(l, i, so[l] + se[l]);
+      sink(l, N - i, so[l] - se[l]);
+    }
   }
   if constexpr (ODD) {
-    double sm[1] = {0.0};
-    dot_rows<H, 1, (H > 0 ? H : 1)>(sM, Mm, o, sm);
-    sink(H, sm[0]);
+    double sm[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) sm[l] = 0.0;
+#pragma unroll
+    for (int m = 0; m + 1 < H; m += 2) {
+      const double2 c2 = sM.pair(Mm + m);
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        sm[l] = fma(c2.x, x[l][N - m], sm[l]);
+        sm[l] = fma(c2.y, x[l][N - m - 1], sm[l]);
+      }
+    }
+    if constexpr (H & 1) {
+      const double cl = sM.one(Mm + H - 1);
+#pragma unroll
+      for (int l = 0; l < L; ++l) sm[l] = fma(cl, x[l][N - (H - 1)], sm[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) sink(l, H, sm[l]);
   }
 }
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = LinesShape<N>::MINB, int EPBX = 0,
           int PFL = LinesShape<N>::PFL_DEF,
           bool GCS = true, int ASM = 0, bool PFN = false, int DCM = LinesShape<N>::DC_DEF,
-          bool STREAM = LinesShape<N>::STREAM>
+          int STREAM = LinesShape<N>::STREAM, bool GIR = LinesShape<N>::GIR>
 __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
@@ -368,19 +422,31 @@ ax_lines(const AxArgs a) {
         else col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
         s_u[S::at(ca, cb, k)] = col[0][k];
       }
-      eo_apply<N, EPBX, 1>(m1, col, gt);
+      if constexpr (STREAM >= 1) eo_apply_sinkL<N, EPBX, 1>(m1, col, [&](int, int i, double v) { gt[0][i] = v; });
+      else eo_apply<N, EPBX, 1>(m1, col, gt);
     }
     __syncthreads();
 
     // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
-    if constexpr (STREAM) {
-      double in[NP];
+    if constexpr (STREAM == 2) {
+      double in[2][NP];
 #pragma unroll
-      for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(m, ca, cb)];
-      eo_apply_sink<N, EPBX>(m2, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+      for (int m = 0; m < NP; ++m) {
+        in[0][m] = s_u[S::at(m, ca, cb)];
+        in[1][m] = s_u[S::at(ca, m, cb)];
+      }
+      eo_apply_sinkL<N, EPBX, 2>(m2, in, [&](int l, int i, double v) {
+        if (l == 0) s_r[S::at(i, ca, cb)] = v;
+        else s_s[S::at(ca, i, cb)] = v;
+      });
+    } else if constexpr (STREAM == 1) {
+      double in[1][NP];
 #pragma unroll
-      for (int m = 0; m < NP; ++m) in[m] = s_u[S::at(ca, m, cb)];
-      eo_apply_sink<N, EPBX>(m2, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
+      for (int m = 0; m < NP; ++m) in[0][m] = s_u[S::at(m, ca, cb)];
+      eo_apply_sinkL<N, EPBX, 1>(m2, in, [&](int, int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+#pragma unroll
+      for (int m = 0; m < NP; ++m) in[0][m] = s_u[S::at(ca, m, cb)];
+      eo_apply_sinkL<N, EPBX, 1>(m2, in, [&](int, int j, double v) { s_s[S::at(ca, j, cb)] = v; });
     } else {
       double in[2][NP], out[2][NP];
 #pragma unroll
@@ -426,14 +492,25 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
-    if constexpr (STREAM) {
-      double in[NP];
+    if constexpr (STREAM == 2) {
+      double in[2][NP];
 #pragma unroll
-      for (int m = 0; m < NP; ++m) in[m] = s_r[S::at(m, ca, cb)];
-      eo_apply_sink<N, EPBX>(m4, in, [&](int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+      for (int m = 0; m < NP; ++m) {
+        in[0][m] = s_r[S::at(m, ca, cb)];
+        in[1][m] = s_s[S::at(ca, m, cb)];
+      }
+      eo_apply_sinkL<N, EPBX, 2>(m4, in, [&](int l, int i, double v) {
+        if (l == 0) s_r[S::at(i, ca, cb)] = v;
+        else s_s[S::at(ca, i, cb)] = v;
+      });
+    } else if constexpr (STREAM == 1) {
+      double in[1][NP];
 #pragma unroll
-      for (int m = 0; m < NP; ++m) in[m] = s_s[S::at(ca, m, cb)];
-      eo_apply_sink<N, EPBX>(m4, in, [&](int j, double v) { s_s[S::at(ca, j, cb)] = v; });
+      for (int m = 0; m < NP; ++m) in[0][m] = s_r[S::at(m, ca, cb)];
+      eo_apply_sinkL<N, EPBX, 1>(m4, in, [&](int, int i, double v) { s_r[S::at(i, ca, cb)] = v; });
+#pragma unroll
+      for (int m = 0; m < NP; ++m) in[0][m] = s_s[S::at(ca, m, cb)];
+      eo_apply_sinkL<N, EPBX, 1>(m4, in, [&](int, int j, double v) { s_s[S::at(ca, j, cb)] = v; });
     } else {
       double in[2][NP], out[2][NP];
 #pragma unroll
@@ -452,6 +529,13 @@ ax_lines(const AxArgs a) {
 
     // ---- P5: t-direction transposed contraction, sum, assembly Z^T
     if (act) {
+      // GIR: the index column is re-read here (L1/L2 hit) instead of held in registers from P1
+      int32_t gr[GIR ? NP : 1];
+      if constexpr (GIR) {
+#pragma unroll
+        for (int k = 0; k < NP; ++k) gr[k] = __ldg(a.idx + e * NP3 + k * NP2 + c);
+      }
+      auto gidx = [&](int k) { if constexpr (GIR) return gr[k]; else return gi[k]; };
       // node k of the (i,j) column: sum the three directions, lambda terms, assembly Z^T
       auto node = [&](int k, double vtk) {
         const int o = S::at(ca, cb, k);
@@ -467,13 +551,13 @@ ax_lines(const AxArgs a) {
           a.yh[e * NP3 + k * NP2 + c] = out;  // y_L
         } else if (interior_ij && k > 0 && k < N) {
           if (!MASSB) out = fma(a.lam, uk, out);  // W = 1 on element-interior nodes
-          a.y[gi[k]] = out;                          // sole contribution: plain store
+          a.y[gidx(k)] = out;                        // sole contribution: plain store
         } else {
-          red_y<HALO>(a, gi[k], out);
+          red_y<HALO>(a, gidx(k), out);
         }
       };
-      if constexpr (STREAM) {
-        eo_apply_sink<N, EPBX>(m5, gt[0], node);
+      if constexpr (STREAM >= 1) {
+        eo_apply_sinkL<N, EPBX, 1>(m5, gt, [&](int, int k, double v) { node(k, v); });
       } else {
         double vt[1][NP];
         eo_apply<N, EPBX, 1>(m5, gt, vt);

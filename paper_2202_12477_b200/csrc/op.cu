@@ -104,10 +104,10 @@ struct AxKernel {
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0,
           int PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false,
-          int DC = hbk::LinesShape<N>::DC_DEF, bool STREAM = hbk::LinesShape<N>::STREAM>
+          int DC = hbk::LinesShape<N>::DC_DEF, int STREAM = hbk::LinesShape<N>::STREAM, bool GIR = false>
 AxKernel make_lines() {
   AxKernel k;
-  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN, DC, STREAM>);
+  k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN, DC, STREAM, GIR>);
   k.block = hbk::LinesShape<N, EPBX>::BLOCK;
   k.epb = hbk::LinesShape<N, EPBX>::EPB;
   k.smem = hbk::LinesShape<N, EPBX>::SMEM;
@@ -194,6 +194,23 @@ AxKernel tune_variant(int v) {
     case 38: return HB_DCV(8);
     case 39: return HB_DCV(14);
 #undef HB_DCV
+    // large N: two-line streamed contractions (STREAM 2), index re-read in P5 (GIR), register targets
+#define HB_SV(ST, GR, REGS) make_lines<N, false, false, 0, tune_minb<N, 0, REGS>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, hbk::LinesShape<N>::DC_DEF, ST, GR>()
+    case 60: return HB_SV(2, false, 255);
+    case 61: return HB_SV(2, false, 128);
+    case 62: return HB_SV(2, true, 128);
+    case 63: return HB_SV(2, true, 168);
+    case 64: return HB_SV(2, false, 168);
+    case 65: return HB_SV(0, false, 255);
+    case 66: return HB_SV(2, true, 96);
+    case 67: return HB_SV(2, true, 112);
+    case 68: return HB_SV(1, true, 128);
+    case 69: return HB_SV(1, false, 128);
+    case 70: return HB_SV(1, true, 168);
+    case 71: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, true>();
+    case 72: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 1, true>();
+    case 73: return make_lines<N, false, false, 0, tune_minb<N, 0, 168>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, false>();
+#undef HB_SV
     case 32: return make_lines<N, false, false, 0, tune_minb<N, 0, 80>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
     case 33: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
     case 34: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
