@@ -71,19 +71,20 @@ struct LinesShape {
   // Line contractions: 0 = two lines (P2, P4) into output arrays; 1 = one line at a time, every
   // output streamed to shared memory / the assembly as it is formed; 2 = two lines streamed (D
   // read once per two lines, no output arrays).  GIR: the index column is re-read in P5 instead of
-  // held in registers from P1.  Streaming frees the registers for two CTAs per SM at N = 11-13:
-  // N = 11 0.78 -> 0.83 and N = 13 0.62 -> 0.69 of peak (2 lines, index re-read, 128 registers),
-  // N = 12 0.69 -> 0.76 (2 lines, 168 registers); at N = 14, 15 the two-CTA forms spill or lose
-  // to one CTA per SM at 255 registers (profiles/r2/bign/)
-  static constexpr int STREAM_T[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 2, 2, 0, 0};
+  // held in registers from P1.  Streaming frees the registers for two CTAs per SM at N = 11, 12:
+  // N = 11 0.78 -> 0.83 isolated, 0.65 -> 0.74 inside the CG (2 lines, index re-read, 128
+  // registers), N = 12 0.69 -> 0.76 / 0.65 -> 0.70 (2 lines, 168 registers).  N = 13 gains in
+  // isolation (0.62 -> 0.69) but loses inside the CG (0.61 -> 0.55) and keeps one uncapped CTA
+  // per SM; at N = 14, 15 the two-CTA forms spill or lose (profiles/r2/bign/)
+  static constexpr int STREAM_T[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 2, 0, 0, 0};
   static constexpr int STREAM = STREAM_T[N];
-  static constexpr bool GIR = N == 11 || N == 13;
+  static constexpr bool GIR = N == 11;
   // Resident CTAs per SM requested from ptxas, from a per-N register target measured on the
   // B200 (0 = no cap, one CTA per SM), capped by shared memory: N = 7 96 registers (10 CTAs per
   // SM; 0.962 vs 0.943 at C3 with 128, profiles/r1b/tune_n7_regs.jsonl); N = 2 80 registers
-  // (0.614 vs 0.607, profiles/r1b/last_ab_n2regs_n13pad.jsonl); N = 12, 13 two CTAs per SM with
-  // the streamed contractions above; N = 14, 15 uncapped
-  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 128, 0, 0};
+  // (0.614 vs 0.607, profiles/r1b/last_ab_n2regs_n13pad.jsonl); N = 12 two CTAs per SM with
+  // the streamed contractions above; N = 13-15 uncapped
+  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 0, 0, 0};
   static constexpr int REGS = REGS_T[N];
   static constexpr int MINB_REG0 = REGS ? 65536 / (BLOCK * REGS) : 1;
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
@@ -369,6 +370,9 @@ ax_lines(const AxArgs a) {
       }
   }
   __syncthreads();
+
+  // P > 1 tolerance mode: iterations after the device-side stop are no-ops (vec.cuh cg_update_p)
+  if (a.cg && a.e_final != 2 && (a.cg->flags & 2)) return;
 
   for (int64_t base = a.e_begin + (int64_t)blockIdx.x * EPB; base < a.e_end; base += (int64_t)gridDim.x * EPB) {
     if constexpr (PF > 0) {

@@ -38,6 +38,8 @@ ax_vertex(const AxArgs a) {
 #pragma unroll
     for (int m = 0; m < 2; ++m) D[i][m] = c_D[N][i * NP + m];
   double en = 0.0;
+  // P > 1 tolerance mode: iterations after the device-side stop are no-ops (vec.cuh cg_update_p)
+  if (a.cg && a.e_final != 2 && (a.cg->flags & 2)) return;
 
   for (int64_t base = a.e_begin + (int64_t)blockIdx.x * EPB; base < a.e_end; base += (int64_t)gridDim.x * EPB) {
     const int64_t ne = (a.e_end - base) < EPB ? (a.e_end - base) : EPB;

@@ -30,12 +30,14 @@ struct CgScalars {
   double pp;       // local p.p (for the lambda term of the fused p.Ap)
   double e_acc;    // element-energy accumulator across the operator launches of one apply
   double rz;       // Jacobi PCG: r_j.z_j (z = M^-1 r), the rho of alpha / beta
-  double spare;
+  double rr_loc;   // r_{j+1}.r_{j+1} from the r update (local; allreduced in place for P > 1),
+                   // published as rr_new by the p update
   double pad;
   int32_t it;        // iteration counter j
   uint32_t ticket;   // last-CTA detection, vector kernels
   uint32_t ticket_e; // last-CTA detection, operator energy
-  int32_t flags;     // bit 0: CG breakdown detected on the device (tolerance-mode graph)
+  int32_t flags;     // bit 0: CG breakdown detected on the device (tolerance mode);
+                     // bit 1: tolerance-mode solve finished (P > 1: later iterations of a chunk are no-ops)
 };
 
 struct AxArgs {

@@ -210,6 +210,8 @@ AxKernel tune_variant(int v) {
     case 71: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, true>();
     case 72: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 1, true>();
     case 73: return make_lines<N, false, false, 0, tune_minb<N, 0, 168>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, false>();
+    case 74: return HB_SV(0, false, 128);  // round-1 N = 11
+    case 75: return HB_SV(1, false, 160);  // round-1 N = 12 (one streamed line)
 #undef HB_SV
     case 32: return make_lines<N, false, false, 0, tune_minb<N, 0, 80>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
     case 33: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
@@ -337,6 +339,9 @@ struct hb_op {
   DevBuf r, p, Ap, xs, partials, e_part, pp_part, rz_part, invd, scal, hist, dot_out, dot_ticket;
   bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
   bool tol_device_loop = true;  // tolerance mode as one graph with a WHILE node (P = 1)
+  // P > 1 tolerance mode: the stop test taken on the device by cg_update_p (eps < 0: none)
+  double tol_eps = -1.0;
+  int32_t tol_max = INT32_MAX;
   bool timing_vec_only = false; // measurement hook: fixed-mode CG without the operator launches
   int variant = 0;      // 0: fused scatter-add (fp64 RED); 1: y_L + CSR gather (deterministic), P = 1
   DevBuf yL, csr_ptr, csr_slots;
@@ -386,6 +391,7 @@ struct hb_op {
     bool operator<(const TolKey& o) const { return std::tie(K, b, x, eps, st) < std::tie(o.K, o.b, o.x, o.eps, o.st); }
   };
   std::map<TolKey, GraphVal> tol_graphs;  // tolerance mode, one CUDA graph with a WHILE node
+  std::map<TolKey, GraphVal> chunk_graphs;  // P > 1 tolerance mode: a chunk of predicated iterations
   std::map<std::tuple<int32_t, const double*, double*>, GraphVal> scat_graphs;  // scattered-storage CG
   double* host_scal = nullptr;  // pinned CgScalars mirror
   // IPC transport (comm kind 1): peer mappings of the buffers this rank writes into
@@ -417,6 +423,7 @@ struct hb_op {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_stream2) cudaStreamDestroy(cap_stream2);
     for (auto& kv : tol_graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : chunk_graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto& kv : scat_graphs) cudaGraphExecDestroy(kv.second.exec);
     if (ev_cap) cudaEventDestroy(ev_cap);
     for (cudaEvent_t e : {ev_pack, ev_halo, ev_haloel, ev_gather, ev_red, ev_red_done}) if (e) cudaEventDestroy(e);
@@ -1259,7 +1266,7 @@ int cg_vec_part1(hb_op* op, double* x, cudaStream_t st) {
   op->launches++;
   CU_TRY(cudaEventRecord(op->ev_red, st));
   CU_TRY(cudaStreamWaitEvent(op->comm_stream, op->ev_red, 0));
-  HB_TRY(allreduce_sum(op, &s->rr_new, op->comm_stream));
+  HB_TRY(allreduce_sum(op, &s->rr_loc, op->comm_stream));
   CU_TRY(cudaEventRecord(op->ev_red_done, op->comm_stream));
   hbk::cg_update_x<<<gv, hbk::VEC_BLOCK, 0, st>>>(x, op->p.as<double>(), n, s);
   op->launches++;
@@ -1277,7 +1284,7 @@ int cg_vec_part2(hb_op* op, cudaStream_t st) {
   HB_TRY(phase_event(op, op->t_p, true, st));
   hbk::cg_update_p<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
       op->p.as<double>(), op->r.as<double>(), op->Ap.as<double>(), n, lam_init(op), op->partials.as<double>(),
-      op->scal.as<hbk::CgScalars>());
+      op->scal.as<hbk::CgScalars>(), op->tol_eps, op->tol_max);
   op->launches++;
   CU_TRY(cudaGetLastError());
   HB_TRY(phase_event(op, op->t_p, false, st));
@@ -1305,6 +1312,8 @@ int ensure_hist(hb_op* op, int32_t K) {
     op->graphs.clear();
     for (auto& kv : op->tol_graphs) cudaGraphExecDestroy(kv.second.exec);
     op->tol_graphs.clear();
+    for (auto& kv : op->chunk_graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->chunk_graphs.clear();
     for (auto& kv : op->scat_graphs) cudaGraphExecDestroy(kv.second.exec);
     op->scat_graphs.clear();
     HB_TRY(op->hist.alloc(need));
@@ -1471,16 +1480,84 @@ int cg_tol(hb_op* op, const double* b, double* x, int32_t max_iters, double eps,
     HB_TRY(cg_vec_part1(op, x, st));
     CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaStreamSynchronize(st));
-    if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_new)) {
+    if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_loc)) {
       set_error("hb_cg_solve: breakdown (p.Ap <= 0 or non-finite) at iteration " + std::to_string(j));
       return HB_ERR_BREAKDOWN;
     }
     HB_TRY(cg_vec_part2(op, st));
     if (direct_mode(op)) HB_TRY(ipc_signal_ready(op, st));
     ++j;
-    rr = hs->rr_new;
+    rr = hs->rr_loc;
   }
   return finish_result(op, j, rr_hist_host, res, st);
+}
+
+// Tolerance mode with P > 1 without a host round trip per iteration: iterations are enqueued in
+// chunks of kTolChunk; cg_update_p takes the loop test on the device (global r.r, so every rank
+// decides alike) and, once the solve has finished, the remaining iterations of the chunk are
+// no-ops (every iteration kernel returns at once; the exchanges and allreduces still run, on
+// values nobody reads: r.r goes through rr_loc, so rr_new is not re-summed).  The host reads the
+// scalars once per chunk.  NCCL: each chunk is one captured graph, replayed; IPC: stream-ordered
+// (its flags carry per-call sequence numbers).
+constexpr int32_t kTolChunk = 8;
+
+int cg_tol_chunked(hb_op* op, const double* b, double* x, int32_t max_iters, double eps, double* rr_hist_host,
+                   hb_cg_result* res, cudaStream_t st) {
+  HB_TRY(ensure_hist(op, max_iters + kTolChunk));
+  hbk::CgScalars* hs = reinterpret_cast<hbk::CgScalars*>(op->host_scal);
+  if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }
+  HB_TRY(cg_init(op, b, x, st));
+  CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  if (!(hs->rr_new > eps) || max_iters == 0) return finish_result(op, 0, rr_hist_host, res, st);
+  struct Restore {
+    hb_op* o;
+    ~Restore() { o->tol_eps = -1.0; o->tol_max = INT32_MAX; }
+  } restore{op};
+  op->tol_eps = eps;
+  op->tol_max = max_iters;
+  cudaGraphExec_t exec = nullptr;
+  if (!is_ipc(op)) {  // one graph per (max_iters, b, x, eps): kTolChunk predicated iterations
+    hb_op::TolKey key{max_iters, b, x, eps, st};
+    auto it = op->chunk_graphs.find(key);
+    if (it == op->chunk_graphs.end()) {
+      const int64_t l0 = op->launches;
+      const bool prof = op->profiling;
+      op->profiling = false;
+      cudaGraph_t graph;
+      cudaStream_t cs = op->cap_stream;
+      CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int status = HB_OK;
+      for (int32_t j = 0; j < kTolChunk && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
+      cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+      op->profiling = prof;
+      if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
+      CU_TRY(ce);
+      cudaGraphExec_t ex;
+      cudaError_t ie = cudaGraphInstantiate(&ex, graph, 0);
+      cudaGraphDestroy(graph);
+      CU_TRY(ie);
+      it = op->chunk_graphs.emplace(key, hb_op::GraphVal{ex, op->launches - l0, 0, 0, 0}).first;
+      op->launches = l0;
+    }
+    exec = it->second.exec;
+  }
+  for (int32_t launched = 0; launched < max_iters; launched += kTolChunk) {
+    if (exec) {
+      CU_TRY(cudaGraphLaunch(exec, st));
+      op->launches += op->chunk_graphs.find(hb_op::TolKey{max_iters, b, x, eps, st})->second.launches;
+    } else {
+      for (int32_t j = 0; j < kTolChunk; ++j) HB_TRY(cg_iteration(op, x, st));
+    }
+    CU_TRY(cudaMemcpyAsync(op->host_scal, op->scal.p, sizeof(hbk::CgScalars), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    if (hs->flags & 2) break;
+  }
+  if (hs->flags & 1) {
+    set_error("hb_cg_solve: breakdown (p.Ap <= 0 or non-finite) at iteration " + std::to_string(hs->it));
+    return HB_ERR_BREAKDOWN;
+  }
+  return finish_result(op, hs->it, rr_hist_host, res, st);
 }
 
 }  // namespace
@@ -1493,6 +1570,8 @@ extern "C" int hb_cg_solve(hb_op* op, const double* b, double* x, int32_t max_it
   cudaStream_t st = (cudaStream_t)stream;
   if (eps < 0) return cg_fixed(op, b, x, max_iters, rr_hist_host, res, st);
   if (op->fused_grid > 0 && op->tol_device_loop) return cg_tol_graph(op, b, x, max_iters, eps, rr_hist_host, res, st);
+  if (op->comm && op->comm->P > 1 && op->tol_device_loop)
+    return cg_tol_chunked(op, b, x, max_iters, eps, rr_hist_host, res, st);
   return cg_tol(op, b, x, max_iters, eps, rr_hist_host, res, st);
 }
 
@@ -1551,6 +1630,8 @@ extern "C" int hb_op_set_variant(hb_op* op, int variant, void* stream) {
     op->graphs.clear();
     for (auto& kv : op->tol_graphs) cudaGraphExecDestroy(kv.second.exec);
     op->tol_graphs.clear();
+    for (auto& kv : op->chunk_graphs) cudaGraphExecDestroy(kv.second.exec);
+    op->chunk_graphs.clear();
   }
   op->variant = variant;
   return HB_OK;
@@ -1938,7 +2019,8 @@ extern "C" int hb_group_cg_solve(hb_group* g, const double* const* b, double* co
   cudaStream_t st = (cudaStream_t)stream;
   const int P = (int)g->ops.size();
   for (int r = 0; r < P; ++r) HB_TRY(ensure_hist(g->ops[r], max_iters));
-  const size_t off_pAp = offsetof(hbk::CgScalars, pAp), off_rrn = offsetof(hbk::CgScalars, rr_new);
+  const size_t off_pAp = offsetof(hbk::CgScalars, pAp), off_rrn = offsetof(hbk::CgScalars, rr_new),
+               off_rrl = offsetof(hbk::CgScalars, rr_loc);
   for (int r = 0; r < P; ++r) HB_TRY(cg_init(g->ops[r], b[r], x[r], st));
   HB_TRY(group_allreduce(g, off_rrn, st));
   hb_op* o0 = g->ops[0];
@@ -1963,7 +2045,7 @@ extern "C" int hb_group_cg_solve(hb_group* g, const double* const* b, double* co
       hbk::cg_update_r<<<vec_grid(std::max<int64_t>(n, 1)), hbk::VEC_BLOCK, 0, st>>>(
           a->r.as<double>(), a->Ap.as<double>(), n, a->partials.as<double>(), a->scal.as<hbk::CgScalars>());
     }
-    HB_TRY(group_allreduce(g, off_rrn, st));
+    HB_TRY(group_allreduce(g, off_rrl, st));
     for (int r = 0; r < P; ++r) {
       hb_op* a = g->ops[r];
       const int64_t n = a->sz.n_owned;
@@ -1972,10 +2054,10 @@ extern "C" int hb_group_cg_solve(hb_group* g, const double* const* b, double* co
     }
     if (eps >= 0) {
       HB_TRY(read0());
-      if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_new)) {
+      if (!(hs->pAp > 0.0) || !std::isfinite(hs->pAp) || !std::isfinite(hs->rr_loc)) {
         set_error("hb_group_cg_solve: breakdown"); return HB_ERR_BREAKDOWN;
       }
-      rr = hs->rr_new;
+      rr = hs->rr_loc;
     }
     for (int r = 0; r < P; ++r) HB_TRY(cg_vec_part2(g->ops[r], st));
     ++j;

@@ -97,6 +97,7 @@ cg_init(const double* __restrict__ b, double* __restrict__ x, double* __restrict
     s->pp = tot;            // local p.p for the P > 1 path (no preconditioner there: p = r)
     s->e_acc = 0.0;
     s->it = 0;
+    s->flags = 0;
   }
 }
 
@@ -172,7 +173,7 @@ cg_update_xr_e(double* __restrict__ x, const double* __restrict__ p, double* __r
     s->pAp = pAp;
     s->rr = rr;
     if (hist) hist[s->it] = rr;
-    s->rr_new = tot;
+    s->rr_loc = tot;
   }
 }
 
@@ -310,6 +311,7 @@ cg_update_fused0(double* __restrict__ x, double* __restrict__ p, double* __restr
       s->rr = rr;
       if (hist) hist[s->it] = rr;
       s->rr_new = rr_new;
+      s->rr_loc = rr_new;
       s->rz = rho_new;
       s->it += 1;
       if constexpr (COND) {
@@ -459,6 +461,7 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
       s->rr = rr;
       if (hist) hist[s->it] = rr;
       s->rr_new = rr_new;
+      s->rr_loc = rr_new;
       s->rz = rho_new;
       s->it += 1;
       if constexpr (COND) {
@@ -472,6 +475,7 @@ cg_update_fused(double* __restrict__ x, double* __restrict__ p, double* __restri
 // run on the communication stream while x += alpha p executes ("hidden behind the AXPY").
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_r(double* __restrict__ r, const double* __restrict__ Ap, int64_t n, double* partials, CgScalars* s) {
+  if (s->flags & 2) return;  // tolerance-mode solve already finished (the rest of the chunk is idle)
   const double pAp = s->pAp;
   const double alpha = (pAp != 0.0) ? s->rr / pAp : 0.0;  // c15 guard
   double acc = 0.0;
@@ -491,11 +495,12 @@ cg_update_r(double* __restrict__ r, const double* __restrict__ Ap, int64_t n, do
     acc = fma(rv, rv, acc);
   }
   double tot;
-  if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_new = tot;
+  if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_loc = tot;
 }
 
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_x(double* __restrict__ x, const double* __restrict__ p, int64_t n, const CgScalars* s) {
+  if (s->flags & 2) return;
   const double pAp = s->pAp;
   const double alpha = (pAp != 0.0) ? s->rr / pAp : 0.0;
   const int64_t n2 = n >> 1;
@@ -509,13 +514,18 @@ cg_update_x(double* __restrict__ x, const double* __restrict__ p, int64_t n, con
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) x[n - 1] = fma(alpha, p[n - 1], x[n - 1]);
 }
 
-// beta = rr_new / rr;  p = r + beta p;  Ap = lam_init p (assembly init of the next apply);
-// partial p.p -> pp (lambda term of the next fused p.Ap); j += 1
+// beta = rr_loc / rr;  p = r + beta p;  Ap = lam_init p (assembly init of the next apply);
+// partial p.p -> pp (lambda term of the next fused p.Ap); rr_new = rr_loc; j += 1.
+// Tolerance mode with P > 1 (eps >= 0; the solve runs in chunks of iterations without host round
+// trips): the last CTA also takes Alg. 1's loop test (while r.r > eps), the iteration cap and
+// the breakdown check (p.Ap <= 0 or non-finite, R4) and sets flags bit 1, after which every
+// iteration kernel of the chunk returns at once (bit 0 as well on breakdown, j not advanced).
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_p(double* __restrict__ p, const double* __restrict__ r, double* __restrict__ Ap,
-            int64_t n, double lam_init, double* partials, CgScalars* s) {
-  const double rr = s->rr;
-  const double beta = (rr != 0.0) ? s->rr_new / rr : 0.0;  // c15 guard
+            int64_t n, double lam_init, double* partials, CgScalars* s, double eps, int32_t max_iters) {
+  if (s->flags & 2) return;
+  const double rr = s->rr, rrn = s->rr_loc;
+  const double beta = (rr != 0.0) ? rrn / rr : 0.0;  // c15 guard
   double acc = 0.0;
   const int64_t n2 = n >> 1;
   double2* p2 = reinterpret_cast<double2*>(p);
@@ -537,7 +547,16 @@ cg_update_p(double* __restrict__ p, const double* __restrict__ r, double* __rest
   double tot;
   if (finish_reduction(acc, partials, &s->ticket, &tot)) {
     s->pp = tot;
+    s->rr_new = rrn;
+    if (eps >= 0.0) {
+      const double pAp = s->pAp;
+      if (!(pAp > 0.0) || !isfinite(pAp) || !isfinite(rrn)) {
+        s->flags |= 3;
+        return;
+      }
+    }
     s->it += 1;
+    if (eps >= 0.0 && (!(rrn > eps) || s->it >= max_iters)) s->flags |= 2;
   }
 }
 

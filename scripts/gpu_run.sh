@@ -32,7 +32,7 @@ for s in $STAGES; do
            timeout 600 python bench.py --N $n --box $b --steps 3 --warmup 3 --no-cpu-baseline --no-c3 >> $O/cg_sweep.jsonl 2>> $O/cgsweep.err
          done; echo "cgsweep done" >> $O/status.txt ;;
     san) for tool in memcheck racecheck; do
-           SAN_CASES=${SAN_CASES:-"2:0,3:1,7:0,8:1,15:0"} SAN_MULTIWAVE=${SAN_MULTIWAVE:-"1,2,7,12,15"} timeout 1800 \
+           SAN_CASES=${SAN_CASES:-"2:0,3:1,7:0,8:1,11:1,13:0,15:0"} SAN_MULTIWAVE=${SAN_MULTIWAVE:-"1,2,7,11,12,13,15"} timeout 1800 \
              compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py > $O/san_$tool.log 2>&1
            echo "san $tool rc=$?" >> $O/status.txt
          done ;;

@@ -28,8 +28,11 @@ for N, mm in [(int(v.split(':')[0]), int(v.split(':')[1])) for v in os.environ.g
     op.cg(b, x, 2)
     if mm == 0:
         op.cg_scattered(b, x, 2)
-        op.set_jacobi(True)
-        op.cg(b, x, 2)
+        try:
+            op.set_jacobi(True)  # needs the fused (cooperative) update: absent under HB_FUSED_UPDATE=0
+            op.cg(b, x, 2)
+        except hb.HBError:
+            pass
     torch.cuda.synchronize()
 # one multi-wave box per operator kernel family (N = 1 vertex kernel; N = 2 multi-element CTAs;
 # N = 7 the bench degree; N = 12 streaming epilogue; N = 15 one uncapped CTA per SM): every CTA
