@@ -98,10 +98,11 @@ struct LinesShape {
   static constexpr int PFL_DEF = PFL_T[N];
   // Folded D from constant memory (uniform-register / constant-bank operands of the DFMAs, no
   // shared-memory broadcast wavefronts) per phase (mask bit 0 P1, 1 P2, 2 P4, 3 P5); 0 = all from
-  // shared memory.  Measured per N (profiles/r2/dc/): all phases +2..16% at N = 2-6, 9 and +11%
-  // at C2 (N = 7); N = 14 P2, P4, P5 only (+5%); at N = 8, 10-13, 15 the constant loads cost
-  // registers (spills at 255) and lose 2-13%
-  static constexpr int DC_T[16] = {0, 0, 15, 15, 15, 15, 15, 14, 0, 15, 0, 0, 0, 0, 14, 0};
+  // shared memory.  Chosen per N from the CG-embedded operator time at the C3 boxes
+  // (profiles/r2/dc/insitu_masks.jsonl): all phases +3..9% at N = 2-7, 9, 10, 12 (C2 operator
+  // 28.2 -> 27.2 us); N = 14 P2, P4, P5 only (+4%); at N = 8, 11, 15 the constant loads cost
+  // registers (spills under the caps) and lose 2-13%; N = 13 P2, P4, P5 only (+5%)
+  static constexpr int DC_T[16] = {0, 0, 15, 15, 15, 15, 15, 15, 0, 15, 15, 0, 15, 14, 14, 0};
   static constexpr int DC_DEF = DC_T[N];
 };
 

@@ -104,7 +104,7 @@ struct AxKernel {
 
 template <int N, bool HALO, bool MASSB, int PF, int MINB = hbk::LinesShape<N>::MINB, int EPBX = 0,
           int PFL = hbk::LinesShape<N>::PFL_DEF, bool GCS = true, int ASM = 0, bool PFN = false,
-          int DC = hbk::LinesShape<N>::DC_DEF, int STREAM = hbk::LinesShape<N>::STREAM, bool GIR = false>
+          int DC = hbk::LinesShape<N>::DC_DEF, int STREAM = hbk::LinesShape<N>::STREAM, bool GIR = hbk::LinesShape<N>::GIR>
 AxKernel make_lines() {
   AxKernel k;
   k.fn = reinterpret_cast<const void*>(&hbk::ax_lines<N, HALO, MASSB, PF, MINB, EPBX, PFL, GCS, ASM, PFN, DC, STREAM, GIR>);
@@ -480,6 +480,7 @@ int launch_ax(hb_op* op, const AxKernel& k, int64_t e0, int64_t e1, const double
   a.e_final = final_launch ? ((op->comm && op->comm->P > 1) || op->grouped ? 1 : 2) : 0;
   int64_t groups = (e1 - e0 + k.epb - 1) / k.epb;
   int grid = (int)std::min<int64_t>(groups, (int64_t)k.grid_max);
+
   if (energy && final_launch) op->last_grid = grid;
   void* args[] = {&a};
   cudaEvent_t e_start = nullptr, e_stop = nullptr;
@@ -951,9 +952,10 @@ static int op_create_impl(const hb_mesh* m, hb_comm* comm, double lambda, cudaSt
     const char* ue = tune_env("HB_UPD_U");
     const char* me = tune_env("HB_UPD_MINB");
     // default: the batched form (first batch in flight during the p.Ap reduction) for vectors that
-    // fit L2 (C2: +1.3%), the single-item form above that (C3 N=7: the batched one is 2.7% slower;
-    // profiles/r1_update_ab.jsonl)
-    const int U = ue ? atoi(ue) : (n <= 8000000 ? 1 : 0), MB = me ? atoi(me) : 2;
+    // fit L2, two double2 per thread per batch at one 512-thread CTA per SM (C2: update 15.1 ->
+    // 14.6 us, CG +0.7%, profiles/r2/vec/c2_update_batch.jsonl); the single-item form above that
+    // (C3 N=7: the batched one is 2.7% slower; profiles/r1_update_ab.jsonl)
+    const int U = ue ? atoi(ue) : (n <= 8000000 ? 2 : 0), MB = me ? atoi(me) : (U == 2 ? 1 : 2);
     auto pick = [&](auto cond) -> const void* {
       constexpr bool C = decltype(cond)::value;
       if (U == 0) return (const void*)&hbk::cg_update_fused0<C>;

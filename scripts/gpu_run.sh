@@ -37,5 +37,7 @@ for s in $STAGES; do
            echo "san $tool rc=$?" >> $O/status.txt
          done ;;
     calib) timeout 300 python scripts/calib.py > $O/calib.json 2>> $O/calib.err; echo "calib rc=$?" >> $O/status.txt ;;
+    big) timeout 900 python bench.py --box 66,66,66 --steps 3 --warmup 3 --no-cpu-baseline --no-c3 > $O/bench_c4_p1.json 2>> $O/bench.err; echo "c4 rc=$?" >> $O/status.txt
+         timeout 900 python bench.py --N 15 --box 50,50,48 --steps 2 --warmup 3 --no-cpu-baseline --no-c3 > $O/bench_c5_p1.json 2>> $O/bench.err; echo "c5 rc=$?" >> $O/status.txt ;;
   esac
 done
