@@ -19,6 +19,8 @@ for s in $STAGES; do
     ref) timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?" >> $O/status.txt ;;
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
            python bench.py --steps 1 --warmup 1 --iters 20 --no-cpu-baseline --no-profile --no-c3 > $O/ncu_launch.log 2>&1; echo "ncu-list rc=$?" >> $O/status.txt
+         timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 400 --csv --log-file $O/launches_warm.csv \
+           python bench.py --steps 1 --warmup 1 --iters 20 --no-cpu-baseline --no-profile --no-c3 > $O/ncu_launch_warm.log 2>&1; echo "ncu-list-warm rc=$?" >> $O/status.txt
          timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ax_ -s 5 -c 1 -o $O/prof_ax_c2 -f \
            python bench.py --steps 1 --warmup 1 --iters 5 --no-cpu-baseline --no-profile --no-c3 > $O/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> $O/status.txt
          timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ax_ -s 5 -c 1 -o $O/prof_ax_c3 -f \
