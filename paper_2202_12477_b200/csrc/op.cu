@@ -339,6 +339,7 @@ struct hb_op {
   DevBuf r, p, Ap, xs, partials, e_part, pp_part, rz_part, invd, scal, hist, dot_out, dot_ticket;
   bool jacobi = false;  // Jacobi-preconditioned CG (P = 1, fused path)
   bool tol_device_loop = true;  // tolerance mode as one graph with a WHILE node (P = 1)
+  bool graph_ok = true;         // P > 1 NCCL: false once capturing the communicator's calls failed
   // P > 1 tolerance mode: the stop test taken on the device by cg_update_p (eps < 0: none)
   double tol_eps = -1.0;
   int32_t tol_max = INT32_MAX;
@@ -1341,29 +1342,42 @@ int finish_result(hb_op* op, int32_t iters, double* rr_hist_host, hb_cg_result* 
 int cg_fixed(hb_op* op, const double* b, double* x, int32_t K, double* rr_hist_host, hb_cg_result* res,
              cudaStream_t st) {
   HB_TRY(ensure_hist(op, K));
-  if (is_ipc(op)) {  // stream-ordered loop: the transport's flags carry per-call sequence numbers
+  auto stream_loop = [&]() -> int {  // stream-ordered loop, no graph
     if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }
     HB_TRY(cg_init(op, b, x, st));
     for (int32_t j = 0; j < K; ++j) HB_TRY(cg_iteration(op, x, st));
     return finish_result(op, K, rr_hist_host, res, st);
-  }
+  };
+  // IPC: the transport's flags carry per-call sequence numbers, so a replayed graph would repeat
+  // stale values; NCCL: graph capture is the default, the stream loop the fallback if capturing
+  // the communicator's calls fails on this system
+  if (is_ipc(op) || !op->graph_ok) return stream_loop();
   hb_op::GraphKey key{K, b, x, op->profiling, op->timing_vec_only, st};
   auto it = op->graphs.find(key);
   if (op->profiling) { op->prof_used = 0; op->prof_seq = 0; op->t_xr.used = 0; op->t_p.used = 0; }  // a profiling graph records into events 0..n-1
   if (it == op->graphs.end()) {
     int64_t l0 = op->launches;
-    cudaGraph_t graph;
+    cudaGraph_t graph = nullptr;
     cudaStream_t cs = op->cap_stream;
     CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     int status = cg_init(op, b, x, cs);
     for (int32_t j = 0; j < K && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
     cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-    if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
-    CU_TRY(ce);
-    cudaGraphExec_t exec;
-    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    CU_TRY(ie);
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ie = cudaErrorUnknown;
+    if (status == HB_OK && ce == cudaSuccess) ie = cudaGraphInstantiate(&exec, graph, 0);
+    if (ce == cudaSuccess && graph) cudaGraphDestroy(graph);
+    if (status != HB_OK || ce != cudaSuccess || ie != cudaSuccess) {
+      op->launches = l0;
+      if (op->comm && op->comm->P > 1) {  // NCCL calls could not be captured: run uncaptured from now on
+        (void)cudaGetLastError();
+        op->graph_ok = false;
+        return stream_loop();
+      }
+      if (status != HB_OK) return status;
+      CU_TRY(ce);
+      CU_TRY(ie);
+    }
     it = op->graphs.emplace(key, hb_op::GraphVal{exec, op->launches - l0, op->prof_used, op->t_xr.used, op->t_p.used}).first;
     op->launches = l0;
   }
@@ -1519,35 +1533,43 @@ int cg_tol_chunked(hb_op* op, const double* b, double* x, int32_t max_iters, dou
   op->tol_eps = eps;
   op->tol_max = max_iters;
   cudaGraphExec_t exec = nullptr;
-  if (!is_ipc(op)) {  // one graph per (max_iters, b, x, eps): kTolChunk predicated iterations
+  int64_t exec_launches = 0;
+  if (!is_ipc(op) && op->graph_ok) {  // one graph per (max_iters, b, x, eps): kTolChunk predicated iterations
     hb_op::TolKey key{max_iters, b, x, eps, st};
     auto it = op->chunk_graphs.find(key);
     if (it == op->chunk_graphs.end()) {
       const int64_t l0 = op->launches;
       const bool prof = op->profiling;
       op->profiling = false;
-      cudaGraph_t graph;
+      cudaGraph_t graph = nullptr;
       cudaStream_t cs = op->cap_stream;
       CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       int status = HB_OK;
       for (int32_t j = 0; j < kTolChunk && status == HB_OK; ++j) status = cg_iteration(op, x, cs);
       cudaError_t ce = cudaStreamEndCapture(cs, &graph);
       op->profiling = prof;
-      if (status != HB_OK) { if (ce == cudaSuccess) cudaGraphDestroy(graph); return status; }
-      CU_TRY(ce);
-      cudaGraphExec_t ex;
-      cudaError_t ie = cudaGraphInstantiate(&ex, graph, 0);
-      cudaGraphDestroy(graph);
-      CU_TRY(ie);
-      it = op->chunk_graphs.emplace(key, hb_op::GraphVal{ex, op->launches - l0, 0, 0, 0}).first;
+      cudaGraphExec_t ex = nullptr;
+      cudaError_t ie = cudaErrorUnknown;
+      if (status == HB_OK && ce == cudaSuccess) ie = cudaGraphInstantiate(&ex, graph, 0);
+      if (ce == cudaSuccess && graph) cudaGraphDestroy(graph);
+      const int64_t captured = op->launches - l0;
       op->launches = l0;
+      if (status == HB_OK && ce == cudaSuccess && ie == cudaSuccess) {
+        it = op->chunk_graphs.emplace(key, hb_op::GraphVal{ex, captured, 0, 0, 0}).first;
+      } else {  // the communicator's calls could not be captured: stream-ordered chunks
+        (void)cudaGetLastError();
+        op->graph_ok = false;
+      }
     }
-    exec = it->second.exec;
+    if (op->graph_ok) {
+      exec = it->second.exec;
+      exec_launches = it->second.launches;
+    }
   }
   for (int32_t launched = 0; launched < max_iters; launched += kTolChunk) {
     if (exec) {
       CU_TRY(cudaGraphLaunch(exec, st));
-      op->launches += op->chunk_graphs.find(hb_op::TolKey{max_iters, b, x, eps, st})->second.launches;
+      op->launches += exec_launches;
     } else {
       for (int32_t j = 0; j < kTolChunk; ++j) HB_TRY(cg_iteration(op, x, st));
     }

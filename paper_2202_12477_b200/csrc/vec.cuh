@@ -101,40 +101,11 @@ cg_init(const double* __restrict__ b, double* __restrict__ x, double* __restrict
   }
 }
 
-// alpha = rr / pAp;  x += alpha p;  r -= alpha Ap;  partial r.r -> rr_new
-__global__ void __launch_bounds__(VEC_BLOCK)
-cg_update_xr(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
-             const double* __restrict__ Ap, int64_t n, double* partials, CgScalars* s) {
-  const double pAp = s->pAp;
-  const double alpha = (pAp != 0.0) ? s->rr / pAp : 0.0;  // c15 guard
-  double acc = 0.0;
-  const int64_t n2 = n >> 1;
-  double2* x2 = reinterpret_cast<double2*>(x);
-  double2* r2 = reinterpret_cast<double2*>(r);
-  const double2* p2 = reinterpret_cast<const double2*>(p);
-  const double2* a2 = reinterpret_cast<const double2*>(Ap);
-  for (int64_t l = (int64_t)blockIdx.x * VEC_BLOCK + threadIdx.x; l < n2; l += (int64_t)gridDim.x * VEC_BLOCK) {
-    double2 xv = x2[l], pv = p2[l], rv = r2[l], av = a2[l];
-    xv.x = fma(alpha, pv.x, xv.x); xv.y = fma(alpha, pv.y, xv.y);
-    rv.x = fma(-alpha, av.x, rv.x); rv.y = fma(-alpha, av.y, rv.y);
-    x2[l] = xv; r2[l] = rv;
-    acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
-  }
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const int64_t l = n - 1;
-    x[l] = fma(alpha, p[l], x[l]);
-    double rv = fma(-alpha, Ap[l], r[l]);
-    r[l] = rv;
-    acc = fma(rv, rv, acc);
-  }
-  double tot;
-  if (finish_reduction(acc, partials, &s->ticket, &tot)) s->rr_new = tot;
-}
-
 // One GPU: the operator left one energy partial per CTA (e_part[0..n_part)); every CTA of
 // this kernel reduces them in the same fixed order, so p.Ap = sum + lambda p.p is identical
-// everywhere without an extra kernel or a fence/atomic in the operator.  Then as
-// cg_update_xr; the last CTA rotates rr <- r_j.r_j, records the history and publishes p.Ap.
+// everywhere without an extra kernel or a fence/atomic in the operator.  Then alpha = rr / p.Ap,
+// x += alpha p, r -= alpha Ap with the CTA partials of r.r; the last CTA rotates rr <- r_j.r_j,
+// records the history, publishes p.Ap and leaves r_{j+1}.r_{j+1} in rr_loc for the p update.
 __global__ void __launch_bounds__(VEC_BLOCK)
 cg_update_xr_e(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
                const double* __restrict__ Ap, int64_t n, const double* __restrict__ e_part, int n_part,
