@@ -466,6 +466,12 @@ def main():
     peak, peak_src = peaks()
     roof = None
     roof_apply_s = None
+    roof_note = None
+    if vec_ms is not None and ms <= vec_ms:
+        # no operator share to attribute (ranks time-sliced on one GPU: the exchanges' waits
+        # dominate both steps) -- report no roofline rather than a negative one
+        roof_note = (f"operator share not measurable: step {ms:.4f} ms <= vector-only step {vec_ms:.4f} ms")
+        vec_ms = None
     if vec_ms is not None:
         mean_s = (ms - vec_ms) * 1e-3 / K
         alg_bytes = ledger.op_bytes_fused(n, NL_loc, 0)
@@ -544,6 +550,7 @@ def main():
                                       "vector_kernels": round(vec_ms / K, 5),
                                       "sum": round(ms / K, 5)} if vec_ms is not None else None),
                "roofline": roof,
+               **({"roofline_note": roof_note} if roof_note else {}),
                "roofline_c3": roof_c3,
                "cpu_baseline": cpu,
                "clocks": clk.summary()}
