@@ -371,7 +371,7 @@ def test_stream_bench_runs(hb):
     assert np.isfinite(v) and v > 1e11
 
 
-@pytest.mark.parametrize("N,mass_mode", [(4, 1), (7, 0), (2, 1)])
+@pytest.mark.parametrize("N,mass_mode", [(4, 1), (7, 0), (2, 1), (11, 1), (12, 0), (13, 0), (13, 1), (14, 0), (15, 0)])
 def test_cg_random_geometry_both_mass_modes(hb, N, mass_mode):
     """CG with random SPD geometric factors (cross terms live) and both mass modes: the
     fused p.Ap (element energy + lambda p.p, or + lambda u.B u in mode 1) must give the
