@@ -51,9 +51,22 @@ struct LinesShape {
                                      {5, 25, 125},    {9, 54, 324},    {7, 52, 369},     {8, 72, 576},
                                      {9, 81, 729},    {10, 101, 1010}, {11, 121, 1331},  {13, 156, 1872},
                                      {13, 169, 2197}, {17, 238, 3332}, {15, 225, 3375},  {16, 256, 4096}};
+#ifdef HB_PAD_ALT
+  // odd element slabs (multi-element CTAs): N = 2 modelled 360 -> 276, N = 4 440 -> 400 shared
+  // wavefronts per CTA (scripts/smem_conflicts.py model)
+  static constexpr int PADX[3] = {N == 2 ? 3 : N == 4 ? 5 : PAD[N][0], N == 2 ? 18 : N == 4 ? 25 : PAD[N][1],
+                                  N == 2 ? 57 : N == 4 ? 137 : PAD[N][2] + (PAD[N][2] & 1)};
+  static constexpr int P1 = PADX[0];
+  static constexpr int P2 = PADX[1];
+  static constexpr int SLAB = PADX[2];
+#else
   static constexpr int P1 = PAD[N][0];
   static constexpr int P2 = PAD[N][1];
   static constexpr int SLAB = PAD[N][2] + (PAD[N][2] & 1);  // doubles per element per buffer (even)
+#endif
+  // the folded D copy in shared memory starts 16-byte aligned (pair loads)
+  static constexpr int DOFF0 = 3 * EPB * SLAB;
+  static constexpr int DOFF = DOFF0 + (DOFF0 & 1);
   __device__ __forceinline__ static int at(int i, int j, int k) {
     if constexpr (N == 7) return k * 72 + j * 8 + (i ^ (((j >> 1) + 4 * (k & 1)) & 7));
     else if constexpr (N == 15) return k * 256 + j * 16 + (i ^ j);
@@ -67,7 +80,7 @@ struct LinesShape {
   static constexpr int CONST = 2 * MAT;               // D and D^T (host-built, g_EO[N])
   static_assert(CONST <= EO_MAX, "folded D table");
   static_assert(CONST == eo_const(N), "packed constant-memory D table");
-  static constexpr size_t SMEM = sizeof(double) * (3 * EPB * SLAB + CONST);
+  static constexpr size_t SMEM = sizeof(double) * (DOFF + CONST);
   // Line contractions: 0 = two lines (P2, P4) into output arrays; 1 = one line at a time, every
   // output streamed to shared memory / the assembly as it is formed; 2 = two lines streamed (D
   // read once per two lines, no output arrays).  GIR: the index column is re-read in P5 instead of
@@ -334,16 +347,6 @@ __global__ void __launch_bounds__(LinesShape<N, EPBX>::BLOCK, MINB)
 ax_lines(const AxArgs a) {
   using S = LinesShape<N, EPBX>;
   constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB, SLAB = S::SLAB;
-  // STREAM 3, 4 (UT3): P1 only gathers; P3 forms the t-derivative from s_u and leaves the
-  // G-mixed gt in s_u, P5 reads it back -- no column array lives across the phases, so the
-  // register peak is the two streamed lines of P2 / P4.  The energy is summed in P3; u is
-  // re-read from x where P5 still needs it (STREAM 3), or (STREAM 4) interior nodes RED onto
-  // the lambda p initialisation as boundary nodes do
-  // (5, 6: the same with one line at a time in P2 / P4)
-  constexpr bool UT3 = STREAM >= 3;
-  constexpr bool IRED = (STREAM == 4 || STREAM == 6) && !MASSB;
-  constexpr int ST = STREAM >= 5 ? 1 : UT3 ? 2 : STREAM;
-  constexpr bool GIRX = GIR || UT3;
   extern __shared__ double smem[];
   const int t = threadIdx.x;
   const int le = t / NP2;
@@ -357,7 +360,7 @@ ax_lines(const AxArgs a) {
   const ConstMat c_D{eo_off(N)}, c_DT{eo_off(N) + S::MAT};
   SmemMat s_D{nullptr}, s_DT{nullptr};
   if constexpr (DCM != 15) {
-    double* sd = smem + 3 * EPB * SLAB;
+    double* sd = smem + S::DOFF;
     for (int q = t; q < S::CONST; q += S::BLOCK) sd[q] = __ldg(&g_EO[N][q]);
     s_D = SmemMat{sd};
     s_DT = SmemMat{sd + S::MAT};
@@ -427,15 +430,7 @@ ax_lines(const AxArgs a) {
     // ---- P1: gather the (i,j) column (Z x) and the t-derivative in registers
     int32_t gi[NP];
     double gt[1][NP];  // ut, later the G-mixed gt
-    if constexpr (UT3) {  // gather only: the t-derivative is formed in P3 from s_u
-#pragma unroll
-      for (int k = 0; k < NP; ++k) gi[k] = (act && ASM != 2) ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        if constexpr (ASM == 2) s_u[S::at(ca, cb, k)] = act ? __ldg(a.xh + e * NP3 + k * NP2 + c) : 0.0;
-        else s_u[S::at(ca, cb, k)] = act ? load_x<HALO>(a, gi[k]) : 0.0;
-      }
-    } else {
+    {
       double col[1][NP];
 #pragma unroll
       for (int k = 0; k < NP; ++k) gi[k] = (act && ASM != 2) ? __ldg(a.idx + e * NP3 + k * NP2 + c) : 0;
@@ -451,7 +446,7 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
-    if constexpr (ST == 2) {
+    if constexpr (STREAM == 2) {
       double in[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
@@ -462,7 +457,7 @@ ax_lines(const AxArgs a) {
         if (l == 0) s_r[S::at(i, ca, cb)] = v;
         else s_s[S::at(ca, i, cb)] = v;
       });
-    } else if constexpr (ST == 1) {
+    } else if constexpr (STREAM == 1) {
       double in[1][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[0][m] = s_u[S::at(m, ca, cb)];
@@ -487,38 +482,7 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P3: metric at the (i,j) column nodes
-    if constexpr (UT3) {
-      // t-derivative of the column from s_u, each node's metric as its ut is formed; G-mixed gt
-      // replaces u in s_u (this thread's own column), the element energy u.(S_e u) =
-      // (Du).G(Du) is summed here
-      const double* Ge = a.G + e * (6 * NP3);
-      double col[1][NP];
-#pragma unroll
-      for (int k = 0; k < NP; ++k) col[0][k] = s_u[S::at(ca, cb, k)];
-      eo_apply_sinkL<N, EPBX, 1>(m1, col, [&](int, int k, double ut) {
-        double grr = 0, grs = 0, grt = 0, gss = 0, gst = 0, gtt = 0;
-        if (act) {
-          if constexpr (g_pairs(N)) {
-            const double2* g2 = reinterpret_cast<const double2*>(Ge + g_off(true, NP2, k, 0, c));
-            const double2 p0 = ldG2<GCS>(g2), p1 = ldG2<GCS>(g2 + NP2), p2 = ldG2<GCS>(g2 + 2 * NP2);
-            grr = p0.x; grs = p0.y; grt = p1.x; gss = p1.y; gst = p2.x; gtt = p2.y;
-          } else {
-            const double* g = Ge + g_off(false, NP2, k, 0, c);
-            grr = ldG<GCS>(g); grs = ldG<GCS>(g + NP2); grt = ldG<GCS>(g + 2 * NP2);
-            gss = ldG<GCS>(g + 3 * NP2); gst = ldG<GCS>(g + 4 * NP2); gtt = ldG<GCS>(g + 5 * NP2);
-          }
-        }
-        const int o = S::at(ca, cb, k);
-        const double ur = s_r[o], us = s_s[o];
-        const double vr = grr * ur + grs * us + grt * ut;
-        const double vs = grs * ur + gss * us + gst * ut;
-        const double vt = grt * ur + gst * us + gtt * ut;
-        s_r[o] = vr;
-        s_s[o] = vs;
-        s_u[o] = vt;
-        en = fma(ur, vr, fma(us, vs, fma(ut, vt, en)));
-      });
-    } else {
+    {
       const double* Ge = a.G + e * (6 * NP3);
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
@@ -546,7 +510,7 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
-    if constexpr (ST == 2) {
+    if constexpr (STREAM == 2) {
       double in[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
@@ -557,7 +521,7 @@ ax_lines(const AxArgs a) {
         if (l == 0) s_r[S::at(i, ca, cb)] = v;
         else s_s[S::at(ca, i, cb)] = v;
       });
-    } else if constexpr (ST == 1) {
+    } else if constexpr (STREAM == 1) {
       double in[1][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) in[0][m] = s_r[S::at(m, ca, cb)];
@@ -584,45 +548,33 @@ ax_lines(const AxArgs a) {
     // ---- P5: t-direction transposed contraction, sum, assembly Z^T
     if (act) {
       // GIR: the index column is re-read here (L1/L2 hit) instead of held in registers from P1
-      int32_t gr[GIRX ? NP : 1];
-      if constexpr (GIRX && ASM != 2) {
+      int32_t gr[GIR ? NP : 1];
+      if constexpr (GIR) {
 #pragma unroll
         for (int k = 0; k < NP; ++k) gr[k] = __ldg(a.idx + e * NP3 + k * NP2 + c);
       }
-      auto gidx = [&](int k) { if constexpr (GIRX) return gr[k]; else return gi[k]; };
-      // u at node k: from s_u, or (UT3: s_u holds gt by now) re-read from x (an L1 / L2 hit)
-      auto uval = [&](int k) {
-        if constexpr (!UT3) return s_u[S::at(ca, cb, k)];
-        else if constexpr (ASM == 2) return __ldg(a.xh + e * NP3 + k * NP2 + c);
-        else return load_x<HALO>(a, gidx(k));
-      };
+      auto gidx = [&](int k) { if constexpr (GIR) return gr[k]; else return gi[k]; };
       // node k of the (i,j) column: sum the three directions, lambda terms, assembly Z^T
       auto node = [&](int k, double vtk) {
         const int o = S::at(ca, cb, k);
         double out = vtk + s_r[o] + s_s[o];
-        if constexpr (!UT3) en = fma(s_u[o], out, en);
+        const double uk = s_u[o];
+        en = fma(uk, out, en);
         if (MASSB) {
-          const double uk = uval(k);
           const double lb = a.lam * __ldg(a.B + e * NP3 + k * NP2 + c) * uk;
           out += lb;
           en = fma(uk, lb, en);
         }
         if constexpr (ASM >= 1) {  // y_L per slot, assembled by a CSR (gather-scatter) kernel
           a.yh[e * NP3 + k * NP2 + c] = out;  // y_L
-        } else if (!IRED && interior_ij && k > 0 && k < N) {
-          if (!MASSB) out = fma(a.lam, uval(k), out);  // W = 1 on element-interior nodes
-          a.y[gidx(k)] = out;                            // sole contribution: plain store
+        } else if (interior_ij && k > 0 && k < N) {
+          if (!MASSB) out = fma(a.lam, uk, out);  // W = 1 on element-interior nodes
+          a.y[gidx(k)] = out;                        // sole contribution: plain store
         } else {
-          // IRED: interior nodes too, onto Ap = lambda p (mass mode 0) / 0 (mode 1)
           red_y<HALO>(a, gidx(k), out);
         }
       };
-      if constexpr (UT3) {
-        double col[1][NP];
-#pragma unroll
-        for (int k = 0; k < NP; ++k) col[0][k] = s_u[S::at(ca, cb, k)];
-        eo_apply_sinkL<N, EPBX, 1>(m5, col, [&](int, int k, double v) { node(k, v); });
-      } else if constexpr (STREAM >= 1) {
+      if constexpr (STREAM >= 1) {
         eo_apply_sinkL<N, EPBX, 1>(m5, gt, [&](int, int k, double v) { node(k, v); });
       } else {
         double vt[1][NP];

@@ -210,21 +210,6 @@ AxKernel tune_variant(int v) {
     case 71: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, true>();
     case 72: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 1, true>();
     case 73: return make_lines<N, false, false, 0, tune_minb<N, 0, 168>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, false>();
-    // UT3: t-derivative formed in P3, gt kept in s_u (3: interior store with u re-read, 4: interior RED)
-    case 80: return HB_SV(3, true, 128);
-    case 81: return HB_SV(4, true, 128);
-    case 82: return HB_SV(3, true, 96);
-    case 83: return HB_SV(4, true, 96);
-    case 84: return HB_SV(3, true, 168);
-    case 85: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15, 3, true>();
-    case 86: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15, 4, true>();
-    case 87: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 3, true>();
-    case 88: return HB_SV(5, true, 128);
-    case 89: return HB_SV(6, true, 128);
-    case 90: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15, 5, true>();
-    case 91: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15, 6, true>();
-    case 92: return HB_SV(5, true, 96);
-    case 93: return HB_SV(6, true, 96);
     case 74: return HB_SV(0, false, 128);  // round-1 N = 11
     case 75: return HB_SV(1, false, 160);  // round-1 N = 12 (one streamed line)
 #undef HB_SV
