@@ -47,23 +47,15 @@ struct LinesShape {
   // Shared-memory layout of one element buffer: (i,j,k) -> doubles.  NP = 8 and NP = 16 use an
   // XOR swizzle that makes all three line orientations conflict free; other N use row / layer
   // padding from an offline bank-conflict search.
-  static constexpr int PAD[16][3] = {{0, 0, 0},       {2, 5, 12},      {3, 12, 42},      {4, 19, 76},
-                                     {5, 25, 125},    {9, 54, 324},    {7, 52, 369},     {8, 72, 576},
-                                     {9, 81, 729},    {10, 101, 1010}, {11, 121, 1331},  {13, 156, 1872},
-                                     {13, 169, 2197}, {17, 238, 3332}, {15, 225, 3375},  {16, 256, 4096}};
-#ifdef HB_PAD_ALT
-  // odd element slabs (multi-element CTAs): N = 2 modelled 360 -> 276, N = 4 440 -> 400 shared
-  // wavefronts per CTA (scripts/smem_conflicts.py model)
-  static constexpr int PADX[3] = {N == 2 ? 3 : N == 4 ? 5 : PAD[N][0], N == 2 ? 18 : N == 4 ? 25 : PAD[N][1],
-                                  N == 2 ? 57 : N == 4 ? 137 : PAD[N][2] + (PAD[N][2] & 1)};
-  static constexpr int P1 = PADX[0];
-  static constexpr int P2 = PADX[1];
-  static constexpr int SLAB = PADX[2];
-#else
+  // Element slabs may be odd (the D copy after them is realigned).  N = 2, 4: odd slabs from the
+  // conflict model (scripts/smem_conflicts.py, wavefronts per CTA: N = 2 360 -> 276, N = 4
+  // 440 -> 400; measured +5% / +3% inside the CG, profiles/r2/pad/)
+  static constexpr int PAD[16][3] = {{0, 0, 0}, {2, 5, 12}, {3, 18, 57}, {4, 19, 76}, {5, 25, 137}, {9, 54, 324},
+                                     {7, 52, 370}, {8, 72, 576}, {9, 81, 730}, {10, 101, 1010}, {11, 121, 1332},
+                                     {13, 156, 1872}, {13, 169, 2198}, {17, 238, 3332}, {15, 225, 3376}, {16, 256, 4096}};
   static constexpr int P1 = PAD[N][0];
   static constexpr int P2 = PAD[N][1];
-  static constexpr int SLAB = PAD[N][2] + (PAD[N][2] & 1);  // doubles per element per buffer (even)
-#endif
+  static constexpr int SLAB = PAD[N][2];  // doubles per element per buffer
   // the folded D copy in shared memory starts 16-byte aligned (pair loads)
   static constexpr int DOFF0 = 3 * EPB * SLAB;
   static constexpr int DOFF = DOFF0 + (DOFF0 & 1);
