@@ -43,7 +43,17 @@ struct LinesShape {
   // measured best with ~128 (profiles/r1_tune.jsonl)
   static constexpr int EPB_DEF = N == 5 ? 128 / NP2 : ((64 / NP2) > 0 ? (64 / NP2) : 1);
   static constexpr int EPB = EPBX > 0 ? EPBX : EPB_DEF;
-  static constexpr int BLOCK = EPB * NP2;
+  // ALN (the N = 6 default; EPBX = 1 selects the blocked mapping): each 7-thread row of columns /
+  // lines occupies 8 lanes (ca = t & 7, lane 7 idle), so the 56 threads still fill two warps
+  // and every half-warp holds exactly two rows; with row pitch 7 and the rows of layer k
+  // rotated by k (see at()) all three orientations are conflict free (model 616 -> 448 shared
+  // wavefronts per element, scripts/smem_conflicts.py).  Inside the CG at the C3 box: 0.70 ->
+  // 0.76 of peak with 80 registers (12 CTAs per SM; profiles/r2/aln/).  The same alignment at
+  // N = 9-14 (rows of 10-15 columns on 16-lane boundaries, pitch 17) and rotated rows at N = 3
+  // measured slower (-3..-40%): extra warps or spills outweigh the conflicts they remove
+  static constexpr bool ALN = (EPBX == -1 || EPBX == 0) && N == 6;
+  static constexpr int RW = 8;
+  static constexpr int BLOCK = ALN ? NP * RW : EPB * NP2;
   // Shared-memory layout of one element buffer: (i,j,k) -> doubles.  NP = 8 and NP = 16 use an
   // XOR swizzle that makes all three line orientations conflict free; other N use row / layer
   // padding from an offline bank-conflict search.
@@ -53,15 +63,19 @@ struct LinesShape {
   static constexpr int PAD[16][3] = {{0, 0, 0}, {2, 5, 12}, {3, 18, 57}, {4, 19, 76}, {5, 25, 137}, {9, 54, 324},
                                      {7, 52, 370}, {8, 72, 576}, {9, 81, 730}, {10, 101, 1010}, {11, 121, 1332},
                                      {13, 156, 1872}, {13, 169, 2198}, {17, 238, 3332}, {15, 225, 3376}, {16, 256, 4096}};
-  static constexpr int P1 = PAD[N][0];
-  static constexpr int P2 = PAD[N][1];
-  static constexpr int SLAB = PAD[N][2];  // doubles per element per buffer
+  static constexpr int P1 = ALN ? 7 : PAD[N][0];
+  static constexpr int P2 = ALN ? 55 : PAD[N][1];
+  static constexpr int SLAB = ALN ? NP * P2 : PAD[N][2];  // doubles per element per buffer
   // the folded D copy in shared memory starts 16-byte aligned (pair loads)
   static constexpr int DOFF0 = 3 * EPB * SLAB;
   static constexpr int DOFF = DOFF0 + (DOFF0 & 1);
   __device__ __forceinline__ static int at(int i, int j, int k) {
     if constexpr (N == 7) return k * 72 + j * 8 + (i ^ (((j >> 1) + 4 * (k & 1)) & 7));
     else if constexpr (N == 15) return k * 256 + j * 16 + (i ^ j);
+    else if constexpr (ALN) {
+      const int v = i + k;
+      return k * 55 + j * 7 + (v >= 7 ? v - 7 : v);  // rows of layer k rotated by k
+    }
     else return k * P2 + j * P1 + i;
   }
   // even/odd folded operator: H = (N+1)/2 row pairs, HE = H (+1 middle column if N+1 odd);
@@ -88,8 +102,9 @@ struct LinesShape {
   // B200 (0 = no cap, one CTA per SM), capped by shared memory: N = 7 96 registers (10 CTAs per
   // SM; 0.962 vs 0.943 at C3 with 128, profiles/r1b/tune_n7_regs.jsonl); N = 2 80 registers
   // (0.614 vs 0.607, profiles/r1b/last_ab_n2regs_n13pad.jsonl); N = 12 two CTAs per SM with
-  // the streamed contractions above; N = 13-15 uncapped
-  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 128, 96, 128, 128, 128, 128, 160, 0, 0, 0};
+  // the streamed contractions above; N = 6 96 (aligned rows: 12 CTAs of 56 threads, 80
+  // registers; 0.758 vs 0.716 blocked at the same target, 0.695 blocked at 128); N = 13-15 uncapped
+  static constexpr int REGS_T[16] = {0, 64, 80, 64, 96, 96, 96, 96, 128, 128, 128, 128, 160, 0, 0, 0};
   static constexpr int REGS = REGS_T[N];
   static constexpr int MINB_REG0 = REGS ? 65536 / (BLOCK * REGS) : 1;
   static constexpr int MINB_REG = MINB_REG0 < 1 ? 1 : (MINB_REG0 > 16 ? 16 : MINB_REG0);
@@ -341,9 +356,14 @@ ax_lines(const AxArgs a) {
   constexpr int NP = S::NP, NP2 = S::NP2, NP3 = S::NP3, EPB = S::EPB, SLAB = S::SLAB;
   extern __shared__ double smem[];
   const int t = threadIdx.x;
-  const int le = t / NP2;
-  const int c = t - le * NP2;
-  const int ca = c % NP, cb = c / NP;  // (i,j) for columns, (j,k) for rows, (i,k) for s-lines
+  constexpr bool ALN = S::ALN;
+  const int le = ALN ? 0 : t / NP2;
+  const int c0 = t - le * NP2;
+  // (i,j) for columns, (j,k) for rows, (i,k) for s-lines
+  const int ca = ALN ? (t & (S::RW - 1)) : c0 % NP;
+  const int cb = ALN ? (t / S::RW) : c0 / NP;
+  const int c = ALN ? ca + NP * cb : c0;
+  const bool lane_ok = !ALN || ca < NP;  // ALN idle lanes: no shared-memory or global access
   double* s_u = smem + (0 * EPB + le) * SLAB;
   double* s_r = smem + (1 * EPB + le) * SLAB;
   double* s_s = smem + (2 * EPB + le) * SLAB;
@@ -392,7 +412,7 @@ ax_lines(const AxArgs a) {
       }
     }
     const int64_t e = base + le;
-    const bool act = (e < a.e_end);
+    const bool act = (e < a.e_end) && lane_ok;
 
     // Early L2 prefetch of this element's geometric factors (consumed in P3, after the
     // gather and two barriers) and of the next element's index block (next P1).
@@ -430,7 +450,7 @@ ax_lines(const AxArgs a) {
       for (int k = 0; k < NP; ++k) {
         if constexpr (ASM == 2) col[0][k] = act ? __ldg(a.xh + e * NP3 + k * NP2 + c) : 0.0;  // x_L
         else col[0][k] = act ? load_x<HALO>(a, gi[k]) : 0.0;
-        s_u[S::at(ca, cb, k)] = col[0][k];
+        if (lane_ok) s_u[S::at(ca, cb, k)] = col[0][k];
       }
       if constexpr (STREAM >= 1) eo_apply_sinkL<N, EPBX, 1>(m1, col, [&](int, int i, double v) { gt[0][i] = v; });
       else eo_apply<N, EPBX, 1>(m1, col, gt);
@@ -438,7 +458,8 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P2: r-line (row owner (j,k) = (ca,cb)) and s-line ((i,k) = (ca,cb)) gradients
-    if constexpr (STREAM == 2) {
+    if (!lane_ok) {
+    } else if constexpr (STREAM == 2) {
       double in[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
@@ -474,7 +495,7 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P3: metric at the (i,j) column nodes
-    {
+    if (lane_ok) {
       const double* Ge = a.G + e * (6 * NP3);
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
@@ -502,7 +523,8 @@ ax_lines(const AxArgs a) {
     __syncthreads();
 
     // ---- P4: transposed contractions along r and s lines, in place (each line has one owner)
-    if constexpr (STREAM == 2) {
+    if (!lane_ok) {
+    } else if constexpr (STREAM == 2) {
       double in[2][NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) {

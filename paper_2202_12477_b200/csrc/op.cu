@@ -210,6 +210,9 @@ AxKernel tune_variant(int v) {
     case 71: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, true>();
     case 72: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 1, true>();
     case 73: return make_lines<N, false, false, 0, tune_minb<N, 0, 168>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 0, 2, false>();
+    // N = 6: the blocked thread mapping (round-1 layout) at the former and the current register target
+    case 100: if constexpr (N == 6) return make_lines<N, false, false, 0, tune_minb<N, 1, 128>(), 1>(); else break;
+    case 101: if constexpr (N == 6) return make_lines<N, false, false, 0, tune_minb<N, 1, 96>(), 1>(); else break;
     case 74: return HB_SV(0, false, 128);  // round-1 N = 11
     case 75: return HB_SV(1, false, 160);  // round-1 N = 12 (one streamed line)
 #undef HB_SV
@@ -217,8 +220,9 @@ AxKernel tune_variant(int v) {
     case 33: return make_lines<N, false, false, 0, tune_minb<N, 0, 96>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
     case 34: return make_lines<N, false, false, 0, tune_minb<N, 0, 128>(), 0, hbk::LinesShape<N>::PFL_DEF, true, 0, false, 15>();
     default:
-      return make_lines<N, false, false, kLinesPF>();
+      break;
   }
+  return make_lines<N, false, false, kLinesPF>();
 }
 
 AxKernel pick_ax_variant(int N, int v) {
