@@ -12,7 +12,7 @@ for nv in ${TUNE_NV}; do
   n=${nv%%:*}; vs=${nv##*:}
   if [ "${n:0:1}" = "p" ]; then n=${n:1}; cp /tmp/plain.so $L/libhipbone_b200.so; tag=plain  # "p<N>": the plain library
   else cp $L/t$n/libhipbone_b200.so $L/libhipbone_b200.so; tag=t$n; fi
-  b=$(python -c "print({1:'120,100,91',2:'184,184,184',3:'122,122,122',4:'92,92,92',5:'73,73,73',6:'61,61,61',7:'52,52,52',8:'46,46,46',9:'41,41,41',10:'37,37,37',11:'33,33,33',12:'31,31,31',13:'28,28,28',14:'26,26,26',15:'24,24,24'}[$n])")
+  b=${BOX:-}; [ -n "$b" ] || b=$(python -c "print({1:'120,100,91',2:'184,184,184',3:'122,122,122',4:'92,92,92',5:'73,73,73',6:'61,61,61',7:'52,52,52',8:'46,46,46',9:'41,41,41',10:'37,37,37',11:'33,33,33',12:'31,31,31',13:'28,28,28',14:'26,26,26',15:'24,24,24'}[$n])")
   for v in ${vs//,/ }; do
     if { [ "$v" != "0" ] || [ "$tag" != "plain" ]; } && [ -z "$NO_PARITY" ]; then
       HB_AX_VARIANT=$v HB_AX_VN=$n timeout 600 python -m pytest -q -x \
@@ -23,7 +23,7 @@ for nv in ${TUNE_NV}; do
       echo "parity $tag n$n v$v rc=$?" >> $O/status.txt
     fi
     for rep in $(seq 1 ${REPS:-1}); do
-      HB_AX_VARIANT=$v HB_AX_VN=$n timeout 600 python bench.py --N $n --box $b --steps 3 --warmup 3 --no-cpu-baseline --no-c3 \
+      HB_AX_VARIANT=$v HB_AX_VN=$n timeout 600 python bench.py --N $n --box $b --steps ${STEPS:-3} --warmup 3 --no-cpu-baseline --no-c3 \
         | sed "s/^{/{\"lib\": \"$tag\", \"variant\": \"$v\", /" >> $O/tune_insitu.jsonl 2>> $O/tune.err
     done
   done
