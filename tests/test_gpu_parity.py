@@ -124,7 +124,7 @@ def test_apply_multiwave_random_geometry(hb, N):
     assert (np.abs(y.cpu().numpy() - yo) / s).max() <= 1e-12
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 7, 9, 15])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 6, 7, 9, 15])  # 2, 4: odd slabs; 6: aligned rows
 @pytest.mark.parametrize("mass_mode,lam", [(0, 0.0), (0, 2.5), (1, 1.0)])
 def test_apply_modes(hb, N, mass_mode, lam):
     box = (2, 3, 1)
@@ -137,7 +137,7 @@ def test_apply_box_geometry_unequal_extents(hb, N):
     check_apply(hb, (4, 1, 2), N, 1.0, 0, False, ext=(1.0, 2.0, 0.5))
 
 
-@pytest.mark.parametrize("N", [1, 15])
+@pytest.mark.parametrize("N", [1, 6, 15])
 def test_apply_single_element(hb, N):
     check_apply(hb, (1, 1, 1), N, 1.0, 0, True, seed=3)
 
@@ -406,7 +406,8 @@ def test_cg_random_geometry_both_mass_modes(hb, N, mass_mode):
     _cg_contract(hf, ho, jo - 1)
 
 
-@pytest.mark.parametrize("box,N,P", [((5, 4, 3), 7, 4), ((6, 3, 5), 2, 6), ((3, 3, 3), 5, 3), ((9, 7, 5), 1, 4)])
+@pytest.mark.parametrize("box,N,P", [((5, 4, 3), 7, 4), ((6, 3, 5), 2, 6), ((3, 3, 3), 5, 3), ((9, 7, 5), 1, 4),
+                                     ((4, 3, 5), 6, 3), ((5, 3, 4), 4, 2)])
 def test_loopback_uneven_partitions_cg(hb, box, N, P):
     """Uneven element splits (remainder layers), several neighbour counts, N=2..7: the split
     apply with per-rank compute/communication streams and the loopback transport (the NCCL
@@ -470,7 +471,7 @@ def test_tolerance_mode_device_graph_matches_host_loop(hb):
     assert j == 7 and len(h) == 8
 
 
-@pytest.mark.parametrize("N,mass_mode", [(2, 1), (3, 0), (5, 1), (7, 0), (8, 1)])  # 2, 7, 8: factor-pair G layout
+@pytest.mark.parametrize("N,mass_mode", [(2, 1), (3, 0), (5, 1), (6, 0), (7, 0), (8, 1)])  # 2, 7, 8: factor-pair G layout
 def test_jacobi_pcg(hb, N, mass_mode):
     """Jacobi-preconditioned CG (NEXT #3): diag(A) against the oracle's assembled element
     diagonals; PCG iterates (fixed and tolerance modes, device-graph and host loops) against
@@ -523,7 +524,7 @@ def test_jacobi_pcg(hb, N, mass_mode):
     _cg_contract(h, hc, min(j, jc, 20))
 
 
-@pytest.mark.parametrize("N,mass_mode", [(3, 0), (7, 1), (10, 0)])
+@pytest.mark.parametrize("N,mass_mode", [(3, 0), (7, 1), (10, 0), (6, 1), (4, 0)])
 def test_deterministic_csr_variant(hb, N, mass_mode):
     """Assembly variant 1 (y_L + CSR gather in ascending (e, n) order): operator parity
     (c17), CG parity (c18), and bitwise reproducibility of repeated applies and solves."""
@@ -560,7 +561,7 @@ def test_deterministic_csr_variant(hb, N, mass_mode):
     _cg_contract(h1, ho, jt - 1)
 
 
-@pytest.mark.parametrize("box,N", [((2, 2, 2), 3), ((5, 4, 3), 7)])
+@pytest.mark.parametrize("box,N", [((2, 2, 2), 3), ((5, 4, 3), 7), ((3, 2, 2), 6)])
 def test_scattered_storage_cg(hb, box, N):
     """NekBone's scattered storage (NEXT #4): CG on x_L = Z x with Z Z^T S_L +
     lambda I and W-weighted dots has the same iterates as the assembled CG (the weighted
